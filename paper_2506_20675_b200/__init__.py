@@ -1,0 +1,466 @@
+"""B200-native MoE verification step (arXiv 2506.20675, "Cascade") — host mirror.
+
+The product is the C ABI in ``include/cascade.h`` implemented by
+``paper_2506_20675_b200/libcascade.so`` (hand-written sm_100a CUDA).  This
+module is the thin Python host mirror of that boundary, used by the tests and
+``bench.py``; it mirrors the reference's error behaviour
+(``std::invalid_argument`` -> ``ValueError``, ``MissingBaselineError``) and its
+geometry vocabulary (``ExpertConfig``: num_layers, experts_per_layer, top_k,
+shared_experts — proj/include/specsim/expert_model.hpp:27-51).
+
+There is no CPU fallback: importing works anywhere, but every call that needs
+the library raises if ``libcascade.so`` is missing, and model creation fails
+loudly without a B200.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field, asdict
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcascade.so")
+
+MAX_TOKENS = 16
+MAX_K = MAX_TOKENS - 1
+
+# tensor kinds (include/cascade_weights.h)
+T_EMBED, T_ATTN_NORM, T_FFN_NORM, T_WQ, T_WK, T_WV, T_WO = 1, 2, 3, 4, 5, 6, 7
+T_ROUTER, T_SHARED_GATE, T_W_GATE, T_W_UP, T_W_DOWN, T_FINAL_NORM, T_LM_HEAD = 8, 9, 10, 11, 12, 13, 14
+
+
+# ----------------------------------------------------------------- errors
+class CascadeError(RuntimeError):
+    """Device or runtime failure (CASCADE_ECUDA / CASCADE_ERUNTIME)."""
+
+
+class MissingBaselineError(RuntimeError):
+    """utility.hpp:52-55 — baseline requested before any k=0 probes."""
+
+
+def _raise(code: int, msg: str):
+    if code == 1:
+        raise ValueError(msg)
+    if code == 4:
+        raise MissingBaselineError(msg)
+    raise CascadeError(msg)
+
+
+# ----------------------------------------------------------------- C structs
+class Geometry(ctypes.Structure):
+    _fields_ = [
+        ("num_layers", ctypes.c_int32),
+        ("experts_per_layer", ctypes.c_int32),
+        ("top_k", ctypes.c_int32),
+        ("shared_experts", ctypes.c_int32),
+        ("d_model", ctypes.c_int32),
+        ("d_ff", ctypes.c_int32),
+        ("n_heads", ctypes.c_int32),
+        ("n_kv_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("vocab", ctypes.c_int32),
+        ("renormalize_topk", ctypes.c_int32),
+        ("shared_gate", ctypes.c_int32),
+        ("rope_theta", ctypes.c_float),
+        ("norm_eps", ctypes.c_float),
+        ("router_scale", ctypes.c_float),
+        ("reserved", ctypes.c_int32 * 5),
+    ]
+
+
+class VerifyOut(ctypes.Structure):
+    _fields_ = [
+        ("accepted", ctypes.c_int32),
+        ("emitted", ctypes.c_int32),
+        ("n_tokens", ctypes.c_int32),
+        ("cache_len", ctypes.c_int32),
+        ("tokens", ctypes.c_int32 * MAX_TOKENS),
+        ("argmax", ctypes.c_int32 * MAX_TOKENS),
+        ("attention_time", ctypes.c_double),
+        ("expert_time", ctypes.c_double),
+        ("draft_time", ctypes.c_double),
+        ("sampling_time", ctypes.c_double),
+        ("active_experts_per_layer", ctypes.c_double),
+        ("total", ctypes.c_double),
+        ("utility", ctypes.c_double),
+        ("verify_ns", ctypes.c_double),
+    ]
+
+
+class DecodeCfg(ctypes.Structure):
+    _fields_ = [
+        ("policy", ctypes.c_int32),
+        ("max_new", ctypes.c_int32),
+        ("ngram_n", ctypes.c_int32),
+        ("t_trial", ctypes.c_int32),
+        ("max_trials", ctypes.c_int32),
+        ("s_set", ctypes.c_int32),
+        ("s_cap", ctypes.c_int32),
+        ("k_max", ctypes.c_int32),
+        ("k_start", ctypes.c_int32),
+        ("convergence_band", ctypes.c_double),
+        ("baseline_refresh_interval", ctypes.c_int32),
+        ("baseline_probe_len", ctypes.c_int32),
+        ("backoff_enabled", ctypes.c_int32),
+        ("injected_cost", ctypes.c_int32),
+        ("cost_by_k", ctypes.c_double * MAX_TOKENS),
+    ]
+
+
+# ----------------------------------------------------------------- geometry presets
+@dataclass
+class ModelShape:
+    """ExpertConfig routing fields + tensor shape (public model configs)."""
+
+    name: str
+    num_layers: int
+    experts_per_layer: int
+    top_k: int
+    shared_experts: int
+    d_model: int
+    d_ff: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    vocab: int
+    renormalize_topk: int = 1
+    shared_gate: int = 0
+    rope_theta: float = 1e6
+    norm_eps: float = 1e-5
+    router_scale: float = 4.0
+
+    def to_c(self) -> Geometry:
+        g = Geometry()
+        for f in Geometry._fields_:
+            if f[0] == "reserved":
+                continue
+            setattr(g, f[0], getattr(self, f[0]))
+        return g
+
+    def with_layers(self, n: int) -> "ModelShape":
+        d = asdict(self)
+        d["num_layers"] = n
+        d["name"] = f"{self.name}-L{n}"
+        return ModelShape(**d)
+
+    # HBM bytes (algorithmic) of one verify step, DESIGN.md §4
+    def step_bytes(self, union_sizes, ctx: int, T: int) -> dict:
+        d, f = self.d_model, self.d_ff
+        hq = self.n_heads * self.head_dim
+        kvd = self.n_kv_heads * self.head_dim
+        expert = 3 * d * f * 2
+        out = {"experts": 0, "dense": 0, "kv": 0, "head": 0}
+        for u in union_sizes:
+            out["experts"] += (u + self.shared_experts) * expert
+            out["dense"] += (d * (hq + 2 * kvd) + hq * d) * 2 + (self.experts_per_layer + self.shared_gate) * d * 2 + 2 * d * 2
+            out["kv"] += ctx * 2 * kvd * 2 + T * 2 * kvd * 2
+        out["head"] = self.vocab * d * 2 + d * 2
+        out["total"] = sum(out.values())
+        return out
+
+
+PRESETS = {
+    # SURVEY.md §8(d) config 1 (authored: the reference has no tiny MoE fixture)
+    "tiny": ModelShape("tiny", 4, 8, 2, 0, 256, 512, 8, 2, 32, 1024, 1, 0, 1e6, 1e-5, 4.0),
+    # config 2: Mixtral-8x7B shape
+    "mixtral": ModelShape("mixtral", 32, 8, 2, 0, 4096, 14336, 32, 8, 128, 32000, 1, 0, 1e6, 1e-5, 4.0),
+    # config 3: OLMoE-1B-7B shape (softmax top-8, no renormalisation)
+    "olmoe": ModelShape("olmoe", 16, 64, 8, 0, 2048, 1024, 16, 16, 128, 50304, 0, 0, 1e4, 1e-5, 4.0),
+    # config 4: Qwen1.5-MoE-A2.7B: 60 routed top-4 + shared expert (5632 = 4 blocks of 1408,
+    # the reference counts it as shared_experts=4, expert_model.hpp:192-193), sigmoid gate
+    "qwen15": ModelShape("qwen15", 24, 60, 4, 4, 2048, 1408, 16, 16, 128, 151936, 0, 1, 1e6, 1e-6, 4.0),
+    # config 5: Mixtral-8x22B shape (281 GB bf16: expert-parallel only)
+    "mixtral8x22b": ModelShape("mixtral8x22b", 56, 8, 2, 0, 6144, 16384, 48, 8, 128, 32768, 1, 0, 1e6, 1e-5, 4.0),
+}
+
+TINY_SEED = 0x5EED
+
+
+def preset(name: str) -> ModelShape:
+    if name not in PRESETS:
+        raise ValueError(f"unknown model preset: {name}")
+    return PRESETS[name]
+
+
+# ----------------------------------------------------------------- library
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libcascade.so (in-tree build).  Raises if it was not built."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i32, i64, u64, dbl, szt = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t
+    sig = {
+        "cascade_last_error": (szt, [ctypes.c_char_p, szt]),
+        "cascade_geometry_validate": (ctypes.c_int, [ctypes.POINTER(Geometry)]),
+        "cascade_model_bytes": (ctypes.c_int, [ctypes.POINTER(Geometry), ctypes.c_int, ctypes.c_int, ctypes.POINTER(u64)]),
+        "cascade_model_create": (ctypes.c_int, [ctypes.POINTER(Geometry), u64, ctypes.c_int, ctypes.POINTER(P)]),
+        "cascade_model_create_ep": (
+            ctypes.c_int,
+            [ctypes.POINTER(Geometry), u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(P)],
+        ),
+        "cascade_model_destroy": (ctypes.c_int, [P]),
+        "cascade_ep_unique_id": (ctypes.c_int, [P, szt]),
+        "cascade_session_create": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(P)]),
+        "cascade_session_destroy": (ctypes.c_int, [P]),
+        "cascade_prefill": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.c_int]),
+        "cascade_session_reset": (ctypes.c_int, [P]),
+        "cascade_set_baseline": (ctypes.c_int, [P, dbl]),
+        "cascade_verify": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.c_int, dbl, ctypes.POINTER(VerifyOut)]),
+        "cascade_last_union_sizes": (ctypes.c_int, [P, ctypes.POINTER(i32), ctypes.c_int]),
+        "cascade_verify_enqueue": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int]),
+        "cascade_sync": (ctypes.c_int, [P]),
+        "cascade_session_stream": (P, [P]),
+        "cascade_step_kernel_count": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "cascade_profile_step": (
+            ctypes.c_int,
+            [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+        ),
+        "cascade_enable_taps": (ctypes.c_int, [P, ctypes.c_int]),
+        "cascade_read_tap": (ctypes.c_int, [P, ctypes.c_int, P, szt]),
+        "cascade_read_weight": (
+            ctypes.c_int,
+            [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_uint16)],
+        ),
+        "cascade_read_kv": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_uint16)]),
+        "cascade_decode": (
+            ctypes.c_int,
+            [
+                P,
+                ctypes.POINTER(i32),
+                ctypes.c_int,
+                ctypes.POINTER(DecodeCfg),
+                ctypes.POINTER(i32),
+                ctypes.POINTER(i32),
+                ctypes.POINTER(dbl),
+                i32,
+                ctypes.POINTER(i32),
+            ],
+        ),
+        "cascade_build_info": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+def last_error() -> str:
+    buf = ctypes.create_string_buffer(4096)
+    lib().cascade_last_error(buf, 4096)
+    return buf.value.decode()
+
+
+def _check(rc: int):
+    if rc != 0:
+        _raise(rc, last_error())
+
+
+def _i32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+# ----------------------------------------------------------------- objects
+class Model:
+    """Random-init weights on one B200 (or one expert-parallel shard)."""
+
+    def __init__(self, shape: ModelShape, seed: int = TINY_SEED, device: int = 0, ep_rank: int = 0, ep_size: int = 1,
+                 nccl_id: Optional[bytes] = None):
+        self.shape = shape
+        self.seed = seed
+        self._g = shape.to_c()
+        h = ctypes.c_void_p()
+        if ep_size == 1:
+            _check(lib().cascade_model_create(ctypes.byref(self._g), seed, device, ctypes.byref(h)))
+        else:
+            idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
+            _check(lib().cascade_model_create_ep(ctypes.byref(self._g), seed, device, ep_rank, ep_size, idbuf,
+                                                 ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().cascade_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def read_weight(self, kind: int, layer: int, expert: int, row0: int, nrows: int, cols: int) -> np.ndarray:
+        out = np.zeros((nrows, cols), np.uint16)
+        _check(lib().cascade_read_weight(self.h, kind, layer, expert, row0, nrows,
+                                         out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16))))
+        return out
+
+
+def ep_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().cascade_ep_unique_id(buf, 128))
+    return buf.raw
+
+
+def model_bytes(shape: ModelShape, ep_rank: int = 0, ep_size: int = 1) -> int:
+    g = shape.to_c()
+    out = ctypes.c_uint64()
+    _check(lib().cascade_model_bytes(ctypes.byref(g), ep_rank, ep_size, ctypes.byref(out)))
+    return out.value
+
+
+def validate_geometry(shape: ModelShape):
+    g = shape.to_c()
+    _check(lib().cascade_geometry_validate(ctypes.byref(g)))
+
+
+KERNEL_CLASSES = ["embed", "qkv", "attention", "attn_combine", "o_proj", "route", "expert_gate_up",
+                  "expert_down", "combine", "lm_head", "accept", "ep_allreduce"]
+
+TAP_KINDS = {
+    "xn_moe": (0, np.uint16, "Ld"),
+    "router_logits": (1, np.float32, "LE1"),
+    "topk_id": (2, np.int32, "Lk"),
+    "topk_w": (3, np.float32, "Lk"),
+    "moe_out": (4, np.float32, "Ld"),
+    "final_logits": (5, np.float32, "V"),
+    "xn_attn": (6, np.uint16, "Ld"),
+    "x_mid": (7, np.float32, "Ld"),
+    "x_in": (8, np.float32, "Ld"),
+}
+
+
+class Session:
+    """One decode request: KV cache + per-width CUDA graphs (cascade_session_*)."""
+
+    def __init__(self, model: Model, max_ctx: int = 2048, k_max: int = 8):
+        self.model = model
+        self.k_max = k_max
+        h = ctypes.c_void_p()
+        _check(lib().cascade_session_create(model.h, max_ctx, k_max, None, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().cascade_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prefill(self, prompt):
+        p = np.ascontiguousarray(prompt, np.int32)
+        _check(lib().cascade_prefill(self.h, _i32p(p), len(p)))
+
+    def reset(self):
+        _check(lib().cascade_session_reset(self.h))
+
+    def set_baseline(self, t_base_ns: float):
+        _check(lib().cascade_set_baseline(self.h, float(t_base_ns)))
+
+    def verify(self, drafts, draft_ns: float = 0.0) -> VerifyOut:
+        d = np.ascontiguousarray(drafts, np.int32)
+        out = VerifyOut()
+        _check(lib().cascade_verify(self.h, _i32p(d) if len(d) else None, len(d), draft_ns, ctypes.byref(out)))
+        return out
+
+    def union_sizes(self) -> np.ndarray:
+        L = self.model.shape.num_layers
+        out = np.zeros(L, np.int32)
+        _check(lib().cascade_last_union_sizes(self.h, _i32p(out), L))
+        return out
+
+    def enqueue(self, K: int, commit: bool = False):
+        _check(lib().cascade_verify_enqueue(self.h, K, 1 if commit else 0))
+
+    def sync(self):
+        _check(lib().cascade_sync(self.h))
+
+    def stream(self) -> int:
+        return lib().cascade_session_stream(self.h) or 0
+
+    def kernel_count(self, K: int) -> int:
+        n = ctypes.c_int()
+        _check(lib().cascade_step_kernel_count(self.h, K, ctypes.byref(n)))
+        return n.value
+
+    def profile(self, K: int):
+        """Per-launch device times (ns) and kernel classes of one eager step."""
+        cap = 64 * self.model.shape.num_layers + 16
+        ns = np.zeros(cap)
+        kind = np.zeros(cap, np.int32)
+        n = ctypes.c_int()
+        _check(lib().cascade_profile_step(self.h, K, ns.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _i32p(kind),
+                                          cap, ctypes.byref(n)))
+        return ns[: n.value], kind[: n.value]
+
+    def enable_taps(self, on: bool = True):
+        _check(lib().cascade_enable_taps(self.h, 1 if on else 0))
+
+    def tap(self, name: str) -> np.ndarray:
+        kind, dt, shp = TAP_KINDS[name]
+        s = self.model.shape
+        L, d, E, k, V = s.num_layers, s.d_model, s.experts_per_layer, s.top_k, s.vocab
+        shape = {"Ld": (L, MAX_TOKENS, d), "LE1": (L, MAX_TOKENS, E + 1), "Lk": (L, MAX_TOKENS, k),
+                 "V": (MAX_TOKENS, V)}[shp]
+        out = np.zeros(shape, dt)
+        _check(lib().cascade_read_tap(self.h, kind, out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out
+
+    def read_kv(self, layer: int, which: int, length: int) -> np.ndarray:
+        s = self.model.shape
+        out = np.zeros((s.n_kv_heads, length, s.head_dim), np.uint16)
+        _check(lib().cascade_read_kv(self.h, layer, which, length, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16))))
+        return out
+
+    def decode(self, prompt, cfg: DecodeCfg, telemetry_cap: int = 0):
+        p = np.ascontiguousarray(prompt, np.int32)
+        out = np.zeros(cfg.max_new + MAX_TOKENS, np.int32)
+        n_out = ctypes.c_int32()
+        n_it = ctypes.c_int32()
+        tel = np.zeros((max(telemetry_cap, 1), 9), np.float64)
+        _check(lib().cascade_decode(self.h, _i32p(p), len(p), ctypes.byref(cfg), _i32p(out), ctypes.byref(n_out),
+                                    tel.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if telemetry_cap else None,
+                                    telemetry_cap, ctypes.byref(n_it)))
+        return out[: n_out.value], tel[: min(n_it.value, telemetry_cap)], n_it.value
+
+
+def decode_cfg(policy: int = -1, max_new: int = 128, ngram_n: int = 3, **controller) -> DecodeCfg:
+    """ControllerConfig defaults of controller.hpp:25-34 (t=4, M=4, S=16, cap=256, k_max=3, k_start=3)."""
+    c = DecodeCfg()
+    c.policy = policy
+    c.max_new = max_new
+    c.ngram_n = ngram_n
+    c.t_trial = controller.get("t_trial", 4)
+    c.max_trials = controller.get("max_trials", 4)
+    c.s_set = controller.get("s_set", 16)
+    c.s_cap = controller.get("s_cap", 256)
+    c.k_max = controller.get("k_max", 3)
+    c.k_start = controller.get("k_start", 3)
+    c.convergence_band = controller.get("convergence_band", 0.10)
+    c.baseline_refresh_interval = controller.get("baseline_refresh_interval", 100)
+    c.baseline_probe_len = controller.get("baseline_probe_len", 4)
+    c.backoff_enabled = 1 if controller.get("backoff_enabled", True) else 0
+    costs = controller.get("cost_by_k")
+    c.injected_cost = 1 if costs is not None else 0
+    if costs is not None:
+        for i, v in enumerate(costs[:MAX_TOKENS]):
+            c.cost_by_k[i] = float(v)
+    return c

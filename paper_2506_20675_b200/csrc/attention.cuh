@@ -1,0 +1,301 @@
+// attention.cuh — causal GQA attention of the T = K+1 in-flight tokens over
+// the request's KV cache, with RoPE and the KV append fused in
+// (SURVEY.md §8(a2) stage K4; replaces the constant attention_time term of
+// iteration_cost, proj/include/specsim/expert_model.hpp:159).
+//
+// Split-KV ("flash-decoding"): work item = (chunk, kv head).  Chunks
+// 0..nch-1 cover the committed cache [0, ctx) in kChunk-key slices; chunk
+// nch is the T new tokens themselves, whose keys/values are rotated,
+// rounded to bf16, appended to the cache and used under the causal mask.
+// All G = H/KV query heads of a KV head share the item (R = G*T rows), so
+// every K/V byte is read once per step.  QK^T and PV run on mma.m16n8k16
+// (bf16 in, fp32 accumulate); one warp owns a 16-row tile and keeps S and
+// O in registers (the S accumulator is re-packed as the P A-fragment).
+// Every item writes (max, sum, unnormalised o) per query row; the combine
+// kernel merges chunks in fixed order and writes the O-projection input in
+// B-frag layout.  ctx is read from device memory, so one captured graph
+// serves every context length.
+#pragma once
+
+#include "common.cuh"
+
+namespace cascade {
+
+constexpr int kChunk = 64;
+constexpr int kAttnThreads = 128;
+constexpr int kAttnMaxRows = 128;  // G * T
+
+struct AttnParams {
+    const float* qkv;        // [T][(H + 2KV) * hd] fp32
+    uint16_t* kc;            // [KV][max_ctx][hd] bf16 (this layer)
+    uint16_t* vc;
+    const int* ctx_ptr;      // committed cache length
+    float* part;             // [KV][R][max_chunks][hd + 2]
+    int T, H, KV, max_ctx, max_chunks;
+    double rope_theta;
+    float scale;             // 1/sqrt(hd)
+};
+
+__device__ __forceinline__ void rope_pair(float& a, float& b, int pos, int i, int hd, double theta) {
+    const double inv = pow(theta, -2.0 * (double)i / (double)hd);
+    double sn, cs;
+    sincos((double)pos * inv, &sn, &cs);
+    const float c = (float)cs, s = (float)sn;
+    const float x0 = a, x1 = b;
+    a = x0 * c - x1 * s;
+    b = x1 * c + x0 * s;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    return (uint32_t)bf16_bits(lo) | ((uint32_t)bf16_bits(hi) << 16);
+}
+
+__device__ __forceinline__ void mma_bf16_regs(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                              uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int HD>
+constexpr int attn_smem_bytes() {
+    return (kAttnMaxRows + 2 * kChunk) * (HD + 8) * 2;
+}
+
+// smem (bf16, row stride HD+8 -> conflict-free fragment loads):
+//   q [kAttnMaxRows][HD+8] | k [kChunk][HD+8] | v [kChunk][HD+8]
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
+    constexpr int LD = HD + 8;
+    constexpr int HALF = HD / 2;
+    constexpr int NKS = HD / 16;      // k-steps of QK^T
+    constexpr int NDT = HD / 8;       // n8 dim tiles of PV
+    extern __shared__ __align__(16) uint16_t sm[];
+    uint16_t* qs = sm;
+    uint16_t* ks = qs + kAttnMaxRows * LD;
+    uint16_t* vs = ks + kChunk * LD;
+
+    const int G = p.H / p.KV;
+    const int R = G * p.T;
+    const int ctx = *p.ctx_ptr;
+    const int nch = (ctx + kChunk - 1) / kChunk;
+    const int n_items = (nch + 1) * p.KV;
+    const int QD = (p.H + 2 * p.KV) * HD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int n_mt = (R + 15) / 16;
+
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int c = item / p.KV;
+        const int kvh = item - c * p.KV;
+        const bool is_new = (c == nch);
+        const int key0 = is_new ? ctx : c * kChunk;
+        const int nkeys = is_new ? p.T : min(kChunk, ctx - key0);
+
+        __syncthreads();
+        // queries (rotated at their own positions, scaled, bf16)
+        for (int e = threadIdx.x; e < n_mt * 16 * HALF; e += blockDim.x) {
+            const int r = e / HALF, i = e - r * HALF;
+            float a = 0.f, b = 0.f;
+            if (r < R) {
+                const int gi = r / p.T, t = r - gi * p.T;
+                const int h = kvh * G + gi;
+                a = p.qkv[(long long)t * QD + h * HD + i];
+                b = p.qkv[(long long)t * QD + h * HD + i + HALF];
+                rope_pair(a, b, ctx + t, i, HD, p.rope_theta);
+                a *= p.scale;
+                b *= p.scale;
+            }
+            qs[r * LD + i] = bf16_bits(a);
+            qs[r * LD + i + HALF] = bf16_bits(b);
+        }
+        if (is_new) {
+            for (int e = threadIdx.x; e < kChunk * HALF; e += blockDim.x) {
+                const int j = e / HALF, i = e - j * HALF;
+                uint16_t ka = 0, kb = 0, va = 0, vb = 0;
+                if (j < p.T) {
+                    const float* kr = p.qkv + (long long)j * QD + p.H * HD + kvh * HD;
+                    const float* vr = p.qkv + (long long)j * QD + (p.H + p.KV) * HD + kvh * HD;
+                    float a = kr[i], b = kr[i + HALF];
+                    rope_pair(a, b, ctx + j, i, HD, p.rope_theta);
+                    ka = bf16_bits(a);
+                    kb = bf16_bits(b);
+                    va = bf16_bits(vr[i]);
+                    vb = bf16_bits(vr[i + HALF]);
+                    const long long base = ((long long)kvh * p.max_ctx + ctx + j) * HD;
+                    p.kc[base + i] = ka;
+                    p.kc[base + i + HALF] = kb;
+                    p.vc[base + i] = va;
+                    p.vc[base + i + HALF] = vb;
+                }
+                ks[j * LD + i] = ka;
+                ks[j * LD + i + HALF] = kb;
+                vs[j * LD + i] = va;
+                vs[j * LD + i + HALF] = vb;
+            }
+        } else {
+            constexpr int V8 = HD / 8;  // uint4 per row
+            const long long base = ((long long)kvh * p.max_ctx + key0) * HD;
+            const uint4* k8 = reinterpret_cast<const uint4*>(p.kc + base);
+            const uint4* v8 = reinterpret_cast<const uint4*>(p.vc + base);
+            for (int e = threadIdx.x; e < kChunk * V8; e += blockDim.x) {
+                const int j = e / V8, q = e - j * V8;
+                uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+                if (j < nkeys) {
+                    kk = __ldg(k8 + e);
+                    vv = __ldg(v8 + e);
+                }
+                *reinterpret_cast<uint4*>(ks + j * LD + q * 8) = kk;
+                *reinterpret_cast<uint4*>(vs + j * LD + q * 8) = vv;
+            }
+        }
+        __syncthreads();
+
+        for (int mt = warp; mt < n_mt; mt += kAttnThreads / 32) {
+            const int r0 = mt * 16;
+            // S = Q K^T  (16 rows x 64 keys)
+            float s[8][4];
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s[n][q] = 0.f;
+#pragma unroll
+            for (int kst = 0; kst < NKS; ++kst) {
+                const int i0 = kst * 16 + 2 * t4;
+                const uint32_t a0 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g) * LD + i0);
+                const uint32_t a1 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0);
+                const uint32_t a2 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g) * LD + i0 + 8);
+                const uint32_t a3 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0 + 8);
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    const uint32_t b0 = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0);
+                    const uint32_t b1 = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0 + 8);
+                    mma_bf16_regs(s[n], a0, a1, a2, a3, b0, b1);
+                }
+            }
+            // mask + row softmax statistics (rows r0+g and r0+g+8)
+            const int ra = r0 + g, rb = r0 + g + 8;
+            const int ta = ra % p.T, tb = rb % p.T;
+            float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = n * 8 + 2 * t4 + (q & 1);
+                    const int tt = (q < 2) ? ta : tb;
+                    const bool ok = j < nkeys && (!is_new || j <= tt);
+                    if (!ok) s[n][q] = -INFINITY;
+                    if (q < 2) ma = fmaxf(ma, s[n][q]);
+                    else mb = fmaxf(mb, s[n][q]);
+                }
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+                mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+            }
+            float la = 0.f, lb = 0.f;
+#pragma unroll
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float m = (q < 2) ? ma : mb;
+                    const float e = (s[n][q] == -INFINITY) ? 0.f : __expf(s[n][q] - m);
+                    s[n][q] = e;
+                    if (q < 2) la += e;
+                    else lb += e;
+                }
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                la += __shfl_xor_sync(0xffffffffu, la, o);
+                lb += __shfl_xor_sync(0xffffffffu, lb, o);
+            }
+            // O = P V  (16 rows x HD)
+            float o[NDT][4];
+#pragma unroll
+            for (int n = 0; n < NDT; ++n)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[n][q] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t a0 = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
+                const uint32_t a1 = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
+                const uint32_t a2 = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
+                const uint32_t a3 = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+#pragma unroll
+                for (int n = 0; n < NDT; n += 2) {
+                    // ldmatrix.x4.trans: lanes 0-15 -> rows of dims n*8, lanes 16-31 -> dims n*8+8
+                    const int jrow = kk * 16 + (lane & 15);
+                    const int col = n * 8 + ((lane >> 4) << 3);
+                    const uint32_t addr =
+                        (uint32_t)__cvta_generic_to_shared(vs + jrow * LD + col);
+                    uint32_t b0, b1, b2, b3;
+                    asm volatile(
+                        "ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                        : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                        : "r"(addr));
+                    mma_bf16_regs(o[n], a0, a1, a2, a3, b0, b1);
+                    mma_bf16_regs(o[n + 1], a0, a1, a2, a3, b2, b3);
+                }
+            }
+            // partials
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int r = half ? rb : ra;
+                if (r >= R) continue;
+                float* out = p.part + (((long long)kvh * R + r) * p.max_chunks + c) * (HD + 2);
+#pragma unroll
+                for (int n = 0; n < NDT; ++n) {
+                    const int i = n * 8 + 2 * t4;
+                    out[2 + i] = o[n][half * 2 + 0];
+                    out[2 + i + 1] = o[n][half * 2 + 1];
+                }
+                if (t4 == 0) {
+                    out[0] = half ? mb : ma;
+                    out[1] = half ? lb : la;
+                }
+            }
+        }
+    }
+}
+
+// Merge chunk partials in fixed order; write bf16 O-proj input (B-frag).
+struct AttnCombineParams {
+    const float* part;
+    const int* ctx_ptr;
+    uint16_t* out_bfrag;   // [H*hd] B-frag
+    float* tap;            // optional fp32 [T][H*hd]
+    int T, H, KV, hd, max_chunks;
+};
+
+__global__ void attn_combine_kernel(AttnCombineParams p) {
+    const int t = blockIdx.x, h = blockIdx.y;
+    const int G = p.H / p.KV;
+    const int kvh = h / G, gi = h - kvh * G;
+    const int R = G * p.T;
+    const int r = gi * p.T + t;
+    const int ctx = *p.ctx_ptr;
+    const int nch = (ctx + kChunk - 1) / kChunk;
+    const float* base = p.part + ((long long)kvh * R + r) * p.max_chunks * (p.hd + 2);
+    float M = -INFINITY;
+    for (int c = 0; c <= nch; ++c) M = fmaxf(M, base[(long long)c * (p.hd + 2)]);
+    float L = 0.f;
+    for (int c = 0; c <= nch; ++c) {
+        const float* b = base + (long long)c * (p.hd + 2);
+        L += b[1] * __expf(b[0] - M);
+    }
+    for (int i = threadIdx.x; i < p.hd; i += blockDim.x) {
+        float o = 0.f;
+        for (int c = 0; c <= nch; ++c) {
+            const float* b = base + (long long)c * (p.hd + 2);
+            o += b[2 + i] * __expf(b[0] - M);
+        }
+        const float v = o / L;
+        const int k = h * p.hd + i;
+        p.out_bfrag[bfrag_index(t, k)] = bf16_bits(v);
+        if (p.tap) p.tap[(long long)t * p.H * p.hd + k] = v;
+    }
+}
+
+}  // namespace cascade

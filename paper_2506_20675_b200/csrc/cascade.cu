@@ -1,0 +1,1196 @@
+// cascade.cu — the C ABI of include/cascade.h: model weights, sessions,
+// the verification-step graph and greedy acceptance.
+//
+// One verification step of width T = K+1:
+//   H2D step params -> embed+norm
+//   per layer: QKV GEMV -> attention (RoPE, KV append, split-KV) -> combine
+//              -> O GEMV (+residual) -> route (norm, router, top-k, union)
+//              -> expert gate/up GEMV (SiLU fused) -> expert down GEMV
+//              -> [EP all-reduce] -> combine (+residual, next norm)
+//   LM head GEMV (+argmax) -> accept (greedy prefix, KV commit, utility)
+//   -> D2H result
+// captured once per T into a CUDA graph; routing, context length and the
+// pending token live in device memory so the graph is replayed unchanged.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "attention.cuh"
+#include "cascade.h"
+#include "common.cuh"
+#include "gemv.cuh"
+#include "init.cuh"
+#include "moe.cuh"
+
+#ifndef CASCADE_GIT
+#define CASCADE_GIT "unknown"
+#endif
+
+using namespace cascade;
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+
+static int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_err(CASCADE_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+extern "C" size_t cascade_last_error(char* buf, size_t n) {
+    if (buf && n) {
+        const size_t c = std::min(n - 1, g_err.size());
+        std::memcpy(buf, g_err.data(), c);
+        buf[c] = 0;
+    }
+    return g_err.size();
+}
+
+extern "C" const char* cascade_build_info(void) { return "sm_100a " CASCADE_GIT; }
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+struct NcclApi {
+    void* h = nullptr;
+    int (*GetUniqueId)(nccl_uid_t*) = nullptr;
+    int (*CommInitRank)(nccl_comm_t*, int, nccl_uid_t, int) = nullptr;
+    int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*CommDestroy)(nccl_comm_t) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+static NcclApi g_nccl;
+static int nccl_load() {
+    if (g_nccl.h) return CASCADE_OK;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return set_err(CASCADE_ERUNTIME, std::string("dlopen libnccl: ") + dlerror());
+    g_nccl.GetUniqueId = (int (*)(nccl_uid_t*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (int (*)(nccl_comm_t*, int, nccl_uid_t, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t))dlsym(
+        h, "ncclAllReduce");
+    g_nccl.CommDestroy = (int (*)(nccl_comm_t))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy)
+        return set_err(CASCADE_ERUNTIME, "libnccl is missing symbols");
+    g_nccl.h = h;
+    return CASCADE_OK;
+}
+constexpr int kNcclFloat32 = 7;
+constexpr int kNcclSum = 0;
+
+extern "C" int cascade_ep_unique_id(void* out, size_t n) {
+    if (!out || n < sizeof(nccl_uid_t)) return set_err(CASCADE_EINVAL, "unique id buffer < 128 bytes");
+    int rc = nccl_load();
+    if (rc) return rc;
+    nccl_uid_t id;
+    if (g_nccl.GetUniqueId(&id) != 0) return set_err(CASCADE_ERUNTIME, "ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+    return CASCADE_OK;
+}
+
+// ---------------------------------------------------------------- geometry
+static int validate(const cascade_geometry* g) {
+    if (!g) return set_err(CASCADE_EINVAL, "geometry is NULL");
+    auto bad = [](const std::string& m) { return set_err(CASCADE_EINVAL, "cascade_geometry: " + m); };
+    // the reference's own ExpertConfig rules (expert_model.hpp:37-50)
+    if (g->num_layers < 1) return bad("num_layers must be >= 1");
+    if (g->top_k < 1 || g->shared_experts < 0 || g->top_k > g->experts_per_layer)
+        return bad("need 1 <= top_k <= experts_per_layer and shared_experts >= 0");
+    // limits of this implementation
+    if (g->num_layers > CASCADE_MAX_LAYERS) return bad("num_layers > 128");
+    if (g->experts_per_layer > kMaxExperts) return bad("experts_per_layer > 128 (expert_model.hpp:96)");
+    if (g->top_k > kMaxTopK) return bad("top_k > 16");
+    if (g->shared_experts > 16) return bad("shared_experts > 16");
+    if (g->d_model < 64 || g->d_model % 64) return bad("d_model must be a positive multiple of 64");
+    if (g->d_ff < 32 || g->d_ff % 32) return bad("d_ff must be a positive multiple of 32");
+    if (g->head_dim != 32 && g->head_dim != 64 && g->head_dim != 128) return bad("head_dim must be 32, 64 or 128");
+    if (g->n_kv_heads < 1 || g->n_heads < 1 || g->n_heads % g->n_kv_heads) return bad("n_heads must be a multiple of n_kv_heads");
+    if ((g->n_heads / g->n_kv_heads) * kMaxT > kAttnMaxRows) return bad("n_heads / n_kv_heads must be <= 8");
+    if ((g->n_heads * g->head_dim) % 64) return bad("n_heads*head_dim must be a multiple of 64");
+    if (((g->n_heads + 2 * g->n_kv_heads) * g->head_dim) % 64) return bad("(H+2KV)*head_dim must be a multiple of 64");
+    if (g->vocab < 64 || g->vocab % 64) return bad("vocab must be a positive multiple of 64");
+    if (!(g->rope_theta > 0.f)) return bad("rope_theta must be > 0");
+    if (!(g->norm_eps > 0.f)) return bad("norm_eps must be > 0");
+    if (!(g->router_scale > 0.f)) return bad("router_scale must be > 0");
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_geometry_validate(const cascade_geometry* g) { return validate(g); }
+
+struct Dims {
+    int L, E, k, S, d, f, H, KV, hd, V, qkvd, hq;
+    long long w13_vec, w2_vec, wqkv_vec, wo_vec, lm_vec;  // uint4 counts
+    explicit Dims(const cascade_geometry& g) {
+        L = g.num_layers; E = g.experts_per_layer; k = g.top_k; S = g.shared_experts;
+        d = g.d_model; f = g.d_ff; H = g.n_heads; KV = g.n_kv_heads; hd = g.head_dim; V = g.vocab;
+        hq = H * hd;
+        qkvd = (H + 2 * KV) * hd;
+        w13_vec = (long long)2 * f * d / 8;
+        w2_vec = (long long)d * f / 8;
+        wqkv_vec = (long long)qkvd * d / 8;
+        wo_vec = (long long)d * hq / 8;
+        lm_vec = (long long)V * d / 8;
+    }
+};
+
+static void local_experts(int E, int rank, int size, int& lo, int& hi) {
+    lo = (int)((long long)E * rank / size);
+    hi = (int)((long long)E * (rank + 1) / size);
+}
+static int local_shared(int S, int rank, int size) {
+    int n = 0;
+    for (int b = 0; b < S; ++b) n += (b % size) == rank;
+    return n;
+}
+
+extern "C" int cascade_model_bytes(const cascade_geometry* g, int ep_rank, int ep_size, uint64_t* out) {
+    int rc = validate(g);
+    if (rc) return rc;
+    if (!out || ep_size < 1 || ep_rank < 0 || ep_rank >= ep_size) return set_err(CASCADE_EINVAL, "bad EP rank/size");
+    Dims D(*g);
+    int lo, hi;
+    local_experts(D.E, ep_rank, ep_size, lo, hi);
+    const long long nb = (hi - lo) + local_shared(D.S, ep_rank, ep_size);
+    uint64_t per_layer = (uint64_t)(D.wqkv_vec + D.wo_vec + nb * (D.w13_vec + D.w2_vec)) * 16 +
+                         (uint64_t)2 * D.d * 2 + (uint64_t)(D.E + 1) * D.d * 2;
+    *out = per_layer * D.L + (uint64_t)D.V * D.d * 2 * 2 + (uint64_t)D.d * 2;
+    return CASCADE_OK;
+}
+
+// ---------------------------------------------------------------- model
+struct LayerW {
+    uint16_t* attn_norm = nullptr;
+    uint16_t* ffn_norm = nullptr;
+    uint16_t* router = nullptr;  // [E + 1][d] (row E = shared gate when present)
+    uint4* wqkv = nullptr;
+    uint4* wo = nullptr;
+    uint4* w13 = nullptr;        // [n_blocks][2f x d]
+    uint4* w2 = nullptr;         // [n_blocks][d x f]
+};
+
+struct cascade_model {
+    cascade_geometry g{};
+    uint64_t seed = 0;
+    int device = 0;
+    int num_sms = 148;
+    int ep_rank = 0, ep_size = 1;
+    int e_lo = 0, e_hi = 0, n_shared_local = 0, n_blocks = 0;
+    std::vector<LayerW> layers;
+    uint16_t* embed = nullptr;
+    uint16_t* final_norm = nullptr;
+    uint4* lm_head = nullptr;
+    std::vector<void*> allocs;
+    uint64_t bytes = 0;
+    nccl_comm_t comm = nullptr;
+};
+
+template <typename T>
+static int dalloc(cascade_model* m, T** p, size_t bytes) {
+    void* v = nullptr;
+    CK(cudaMalloc(&v, bytes));
+    m->allocs.push_back(v);
+    m->bytes += bytes;
+    *p = (T*)v;
+    return CASCADE_OK;
+}
+
+static uint64_t key_of(const cascade_model* m, int kind, int layer, int expert) {
+    return cascade_tensor_key(m->seed, cascade_tensor_id(kind, layer, expert));
+}
+
+static int init_afrag(cascade_model* m, uint4* dst, int rows, int cols, int rowmap, int k0, int k1, int k2,
+                      int layer, int expert, int n0 = 0, int n1 = 0) {
+    InitParams p{};
+    p.dst = dst;
+    p.n_vec = (long long)rows * cols / 8;
+    p.n_ks = cols / 16;
+    p.rowmap = rowmap;
+    p.n0 = n0;
+    p.n1 = n1;
+    p.cols = cols;
+    const int kinds[3] = {k0, k1, k2};
+    for (int i = 0; i < 3; ++i) {
+        const int kd = kinds[i] ? kinds[i] : k0;
+        p.key[i] = key_of(m, kd, layer, expert);
+        p.scale[i] = cascade_kind_scale(kd, cols, m->g.router_scale);
+    }
+    const int blocks = (int)std::min<long long>((p.n_vec + 255) / 256, (long long)m->num_sms * 16);
+    init_afrag_kernel<<<blocks, 256>>>(p);
+    CK(cudaGetLastError());
+    return CASCADE_OK;
+}
+
+static int init_plain(cascade_model* m, uint16_t* dst, int rows, int cols, int kind, int layer, int expert,
+                      int fan_in) {
+    const long long n = (long long)rows * cols;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)m->num_sms * 16);
+    init_plain_kernel<<<blocks, 256>>>(dst, n, cols, n, key_of(m, kind, layer, expert),
+                                       cascade_kind_scale(kind, fan_in, m->g.router_scale), 0);
+    CK(cudaGetLastError());
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_model_destroy(cascade_model* m) {
+    if (!m) return CASCADE_OK;
+    cudaSetDevice(m->device);
+    cudaDeviceSynchronize();
+    for (void* p : m->allocs) cudaFree(p);
+    if (m->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(m->comm);
+    delete m;
+    return CASCADE_OK;
+}
+
+static int model_create(const cascade_geometry* g, uint64_t seed, int device, int ep_rank, int ep_size,
+                        const void* uid, cascade_model** out) {
+    int rc = validate(g);
+    if (rc) return rc;
+    if (!out) return set_err(CASCADE_EINVAL, "out is NULL");
+    if (ep_size < 1 || ep_rank < 0 || ep_rank >= ep_size) return set_err(CASCADE_EINVAL, "bad EP rank/size");
+    if (ep_size > g->experts_per_layer) return set_err(CASCADE_EINVAL, "ep_size > experts_per_layer");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return set_err(CASCADE_EINVAL, "device index out of range");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return set_err(CASCADE_ERUNTIME, "this library is built for sm_100a (B200)");
+
+    cascade_model* m = new cascade_model();
+    m->g = *g;
+    m->seed = seed;
+    m->device = device;
+    m->num_sms = prop.multiProcessorCount;
+    m->ep_rank = ep_rank;
+    m->ep_size = ep_size;
+    local_experts(g->experts_per_layer, ep_rank, ep_size, m->e_lo, m->e_hi);
+    m->n_shared_local = local_shared(g->shared_experts, ep_rank, ep_size);
+    m->n_blocks = (m->e_hi - m->e_lo) + m->n_shared_local;
+    Dims D(*g);
+    m->layers.resize(D.L);
+
+    auto fail = [&](int code) {
+        std::string msg = g_err;
+        cascade_model_destroy(m);
+        g_err = msg;
+        return code;
+    };
+
+    for (int l = 0; l < D.L; ++l) {
+        LayerW& w = m->layers[l];
+        if ((rc = dalloc(m, &w.attn_norm, D.d * 2)) || (rc = dalloc(m, &w.ffn_norm, D.d * 2)) ||
+            (rc = dalloc(m, &w.router, (size_t)(D.E + 1) * D.d * 2)) ||
+            (rc = dalloc(m, &w.wqkv, D.wqkv_vec * 16)) || (rc = dalloc(m, &w.wo, D.wo_vec * 16)) ||
+            (rc = dalloc(m, &w.w13, (size_t)m->n_blocks * D.w13_vec * 16)) ||
+            (rc = dalloc(m, &w.w2, (size_t)m->n_blocks * D.w2_vec * 16)))
+            return fail(rc);
+        if ((rc = init_plain(m, w.attn_norm, 1, D.d, CASCADE_T_ATTN_NORM, l, 0, D.d)) ||
+            (rc = init_plain(m, w.ffn_norm, 1, D.d, CASCADE_T_FFN_NORM, l, 0, D.d)) ||
+            (rc = init_plain(m, w.router, D.E, D.d, CASCADE_T_ROUTER, l, 0, D.d)))
+            return fail(rc);
+        if (g->shared_gate) {
+            if ((rc = init_plain(m, w.router + (size_t)D.E * D.d, 1, D.d, CASCADE_T_SHARED_GATE, l, 0, D.d)))
+                return fail(rc);
+        } else {
+            CK(cudaMemset(w.router + (size_t)D.E * D.d, 0, D.d * 2));
+        }
+        if ((rc = init_afrag(m, w.wqkv, D.qkvd, D.d, ROWMAP_QKV, CASCADE_T_WQ, CASCADE_T_WK, CASCADE_T_WV, l, 0,
+                             D.hq, D.KV * D.hd)) ||
+            (rc = init_afrag(m, w.wo, D.d, D.hq, ROWMAP_SIMPLE, CASCADE_T_WO, 0, 0, l, 0)))
+            return fail(rc);
+        for (int b = 0; b < m->n_blocks; ++b) {
+            // global expert index: local routed experts, then local shared blocks
+            int ge;
+            if (b < m->e_hi - m->e_lo) {
+                ge = m->e_lo + b;
+            } else {
+                int lb = b - (m->e_hi - m->e_lo), seen = 0;
+                ge = -1;
+                for (int s = 0; s < D.S; ++s)
+                    if (s % ep_size == ep_rank) {
+                        if (seen == lb) { ge = D.E + s; break; }
+                        ++seen;
+                    }
+            }
+            if ((rc = init_afrag(m, w.w13 + (size_t)b * D.w13_vec, 2 * D.f, D.d, ROWMAP_GATEUP, CASCADE_T_W_GATE,
+                                 CASCADE_T_W_UP, 0, l, ge)) ||
+                (rc = init_afrag(m, w.w2 + (size_t)b * D.w2_vec, D.d, D.f, ROWMAP_SIMPLE, CASCADE_T_W_DOWN, 0, 0,
+                                 l, ge)))
+                return fail(rc);
+        }
+    }
+    if ((rc = dalloc(m, &m->embed, (size_t)D.V * D.d * 2)) || (rc = dalloc(m, &m->final_norm, D.d * 2)) ||
+        (rc = dalloc(m, &m->lm_head, D.lm_vec * 16)))
+        return fail(rc);
+    if ((rc = init_plain(m, m->embed, D.V, D.d, CASCADE_T_EMBED, 0, 0, D.d)) ||
+        (rc = init_plain(m, m->final_norm, 1, D.d, CASCADE_T_FINAL_NORM, 0, 0, D.d)) ||
+        (rc = init_afrag(m, m->lm_head, D.V, D.d, ROWMAP_SIMPLE, CASCADE_T_LM_HEAD, 0, 0, 0, 0)))
+        return fail(rc);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        set_err(CASCADE_ECUDA, std::string("weight init: ") + cudaGetErrorString(e));
+        return fail(CASCADE_ECUDA);
+    }
+    if (ep_size > 1) {
+        if ((rc = nccl_load())) return fail(rc);
+        if (!uid) {
+            set_err(CASCADE_EINVAL, "nccl_unique_id is NULL for ep_size > 1");
+            return fail(CASCADE_EINVAL);
+        }
+        nccl_uid_t id;
+        std::memcpy(&id, uid, sizeof(id));
+        const int nr = g_nccl.CommInitRank(&m->comm, ep_size, id, ep_rank);
+        if (nr != 0) {
+            set_err(CASCADE_ERUNTIME, std::string("ncclCommInitRank: ") +
+                                          (g_nccl.GetErrorString ? g_nccl.GetErrorString(nr) : "error"));
+            m->comm = nullptr;
+            return fail(CASCADE_ERUNTIME);
+        }
+    }
+    *out = m;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_model_create(const cascade_geometry* g, uint64_t seed, int device, cascade_model** out) {
+    return model_create(g, seed, device, 0, 1, nullptr, out);
+}
+
+extern "C" int cascade_model_create_ep(const cascade_geometry* g, uint64_t seed, int device, int ep_rank,
+                                       int ep_size, const void* uid, cascade_model** out) {
+    return model_create(g, seed, device, ep_rank, ep_size, uid, out);
+}
+
+// ---------------------------------------------------------------- accept
+struct AcceptParams {
+    const StepParams* sp;
+    DevState* st;
+    unsigned long long* keys;
+    const int* tokens_used;
+    const unsigned long long* stamps;  // [0] start, [1+2l] attn l, [2+2l] moe l, [1+2L] lm head
+    const int* union_size;
+    cascade_verify_out* res;
+    int T, L, S;
+};
+
+__global__ void accept_kernel(AcceptParams p) {
+    if (threadIdx.x != 0) return;
+    const uint64_t t_end = globaltimer();
+    cascade_verify_out r;
+    memset(&r, 0, sizeof(r));
+    int am[kMaxT];
+    for (int t = 0; t < p.T; ++t) {
+        am[t] = argmax_key_index(p.keys[t]);
+        p.keys[t] = 0ull;
+        r.argmax[t] = am[t];
+    }
+    const StepParams sp = *p.sp;
+    int acc = 0;
+    if (sp.mode == 0) {
+        while (acc < p.T - 1 && am[acc] == p.tokens_used[acc + 1]) ++acc;
+        for (int i = 0; i < acc; ++i) r.tokens[i] = p.tokens_used[i + 1];
+        r.tokens[acc] = am[acc];
+        r.accepted = acc;
+        r.emitted = acc + 1;
+        if (sp.commit) {
+            p.st->cache_len += acc + 1;
+            p.st->pending = am[acc];
+        }
+    } else {
+        r.accepted = 0;
+        r.emitted = 0;
+        if (sp.commit) p.st->cache_len += p.T;
+    }
+    p.st->steps += 1;
+    r.n_tokens = p.T;
+    r.cache_len = p.st->cache_len;
+    const double t0 = (double)p.stamps[0];
+    double att = (double)p.stamps[1] - t0, exp_t = 0.0;
+    double active = 0.0;
+    for (int l = 0; l < p.L; ++l) {
+        const double a = (double)p.stamps[1 + 2 * l];
+        const double mo = (double)p.stamps[2 + 2 * l];
+        const double nx = (double)p.stamps[1 + 2 * (l + 1)];  // next attn start or LM head start
+        att += mo - a;
+        exp_t += nx - mo;
+        active += (double)(p.union_size[l] + p.S);
+    }
+    r.attention_time = att;
+    r.expert_time = exp_t;
+    r.sampling_time = (double)t_end - (double)p.stamps[1 + 2 * p.L];
+    r.draft_time = sp.draft_ns;
+    r.total = r.attention_time + r.expert_time + r.draft_time + r.sampling_time;
+    r.active_experts_per_layer = active / p.L;
+    r.verify_ns = (double)t_end - t0;
+    r.utility = (sp.t_base_ns > 0.0 && r.emitted > 0) ? (double)r.emitted * sp.t_base_ns / r.total : 0.0;
+    *p.res = r;
+}
+
+// ---------------------------------------------------------------- session
+struct Taps {
+    uint16_t* xn_moe = nullptr;   // [L][16][d]
+    float* logits = nullptr;      // [L][16][E+1]
+    int* topk_id = nullptr;       // [L][16][k]
+    float* topk_w = nullptr;      // [L][16][k]
+    float* moe_out = nullptr;     // [L][16][d]
+    float* final_logits = nullptr;// [16][V]
+    uint16_t* xn_attn = nullptr;  // [L][16][d]
+    float* x_mid = nullptr;       // [L][16][d] residual after attention
+    float* x_in = nullptr;        // [L][16][d] residual entering the layer
+};
+
+struct cascade_session {
+    cascade_model* m = nullptr;
+    int max_ctx = 0, k_max = 0, max_chunks = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::vector<void*> allocs;
+    StepParams* d_params = nullptr;
+    StepParams* h_params = nullptr;
+    DevState* d_state = nullptr;
+    cascade_verify_out* d_result = nullptr;
+    cascade_verify_out* h_result = nullptr;
+    float* x = nullptr;
+    uint16_t* xn = nullptr;
+    float* qkv = nullptr;
+    float* attn_part = nullptr;
+    uint16_t* attn_out = nullptr;
+    float* logits_router = nullptr;
+    int* ticket = nullptr;
+    int* topk_id = nullptr;
+    float* topk_w = nullptr;
+    float* gsh = nullptr;
+    int* list = nullptr;
+    int* count = nullptr;
+    int* route_rank = nullptr;
+    int* union_size = nullptr;
+    uint16_t* hbuf = nullptr;
+    float* ycontrib = nullptr;
+    float4* partial = nullptr;
+    int* counters = nullptr;
+    unsigned long long* keys = nullptr;
+    unsigned long long* stamps = nullptr;
+    int* tokens_used = nullptr;
+    uint16_t* kc = nullptr;
+    uint16_t* vc = nullptr;
+    float* logits_full = nullptr;  // taps only
+    cudaGraphExec_t graph[kMaxT + 1] = {};
+    int graph_kernels[kMaxT + 1] = {};
+    bool taps_on = false;
+    Taps taps;
+    int gemv_grid = 0;
+    double t_base_ns = 0.0;
+};
+
+template <typename T>
+static int salloc(cascade_session* s, T** p, size_t bytes, bool zero = true) {
+    void* v = nullptr;
+    CK(cudaMalloc(&v, bytes));
+    s->allocs.push_back(v);
+    if (zero) CK(cudaMemset(v, 0, bytes));
+    *p = (T*)v;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_session_destroy(cascade_session* s) {
+    if (!s) return CASCADE_OK;
+    cudaSetDevice(s->m->device);
+    cudaStreamSynchronize(s->stream);
+    for (auto& g : s->graph)
+        if (g) cudaGraphExecDestroy(g);
+    for (void* p : s->allocs) cudaFree(p);
+    if (s->h_params) cudaFreeHost(s->h_params);
+    if (s->h_result) cudaFreeHost(s->h_result);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, void* stream,
+                                      cascade_session** out) {
+    if (!m || !out) return set_err(CASCADE_EINVAL, "model/out is NULL");
+    if (max_ctx < 1) return set_err(CASCADE_EINVAL, "max_ctx must be >= 1");
+    if (k_max < 0 || k_max > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "k_max must be in [0, 15]");
+    CK(cudaSetDevice(m->device));
+    cascade_session* s = new cascade_session();
+    s->m = m;
+    s->max_ctx = max_ctx + kMaxT;  // room for the in-flight rows
+    s->k_max = k_max;
+    s->max_chunks = (s->max_ctx + kChunk - 1) / kChunk + 1;
+    if (stream) {
+        s->stream = (cudaStream_t)stream;
+    } else {
+        cudaError_t e = cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            delete s;
+            return set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+        }
+        s->own_stream = true;
+    }
+    const Dims D(m->g);
+    const int G = D.H / D.KV;
+    const int nslots = m->n_blocks;
+    s->gemv_grid = m->num_sms * 2;
+    const long long workers = (long long)s->gemv_grid * kGemvWarps;
+    long long max_units = std::max<long long>({(long long)D.qkvd / kSTRows, (long long)D.d / kSTRows,
+                                               (long long)nslots * (2 * D.f) / kSTRows,
+                                               (long long)nslots * D.d / kSTRows, (long long)D.V / kSTRows});
+    int rc;
+    auto fail = [&](int code) {
+        std::string msg = g_err;
+        cascade_session_destroy(s);
+        g_err = msg;
+        return code;
+    };
+    if ((rc = salloc(s, &s->d_params, sizeof(StepParams))) || (rc = salloc(s, &s->d_state, sizeof(DevState))) ||
+        (rc = salloc(s, &s->d_result, sizeof(cascade_verify_out))) ||
+        (rc = salloc(s, &s->x, (size_t)kMaxT * D.d * 4)) || (rc = salloc(s, &s->xn, (size_t)D.d * 32)) ||
+        (rc = salloc(s, &s->qkv, (size_t)kMaxT * D.qkvd * 4)) ||
+        (rc = salloc(s, &s->attn_part, (size_t)D.KV * G * kMaxT * s->max_chunks * (D.hd + 2) * 4)) ||
+        (rc = salloc(s, &s->attn_out, (size_t)D.hq * 32)) ||
+        (rc = salloc(s, &s->logits_router, (size_t)kMaxT * (D.E + 1) * 4)) ||
+        (rc = salloc(s, &s->ticket, 4)) || (rc = salloc(s, &s->topk_id, (size_t)kMaxT * D.k * 4)) ||
+        (rc = salloc(s, &s->topk_w, (size_t)kMaxT * D.k * 4)) || (rc = salloc(s, &s->gsh, kMaxT * 4)) ||
+        (rc = salloc(s, &s->list, (size_t)(nslots + 1) * 4)) || (rc = salloc(s, &s->count, 4)) ||
+        (rc = salloc(s, &s->route_rank, (size_t)(nslots + 1) * kMaxT * 4)) ||
+        (rc = salloc(s, &s->union_size, (size_t)D.L * 4)) ||
+        (rc = salloc(s, &s->hbuf, (size_t)std::max(nslots, 1) * D.f * 32)) ||
+        (rc = salloc(s, &s->ycontrib, (size_t)kMaxT * (D.k + D.S) * D.d * 4)) ||
+        (rc = salloc(s, &s->partial, (size_t)workers * 2 * kTPW * 2 * 32 * 16, false)) ||
+        (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
+        (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
+        (rc = salloc(s, &s->kc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)) ||
+        (rc = salloc(s, &s->vc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)))
+        return fail(rc);
+    cudaError_t e = cudaHostAlloc(&s->h_params, sizeof(StepParams), cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&s->h_result, sizeof(cascade_verify_out), cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+        set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+        return fail(CASCADE_ECUDA);
+    }
+    std::memset(s->h_params, 0, sizeof(StepParams));
+    std::memset(s->h_result, 0, sizeof(cascade_verify_out));
+    // attention smem opt-in
+    const int asmem = D.hd == 32 ? attn_smem_bytes<32>() : D.hd == 64 ? attn_smem_bytes<64>() : attn_smem_bytes<128>();
+    if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+    else if (D.hd == 64) e = cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+    else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+    if (e == cudaSuccess && D.d * 4 > 48 * 1024)
+        e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D.d * 4);
+    if (e != cudaSuccess) {
+        set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+        return fail(CASCADE_ECUDA);
+    }
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+        return fail(CASCADE_ECUDA);
+    }
+    *out = s;
+    return CASCADE_OK;
+}
+
+extern "C" void* cascade_session_stream(cascade_session* s) { return s ? (void*)s->stream : nullptr; }
+
+// ------------------------------------------------------------ step enqueue
+template <int NT>
+static void launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaStream_t st) {
+    switch (epi) {
+    case EPI_STORE: stream_gemv_kernel<NT, EPI_STORE><<<grid, kGemvThreads, 0, st>>>(p); break;
+    case EPI_ADD: stream_gemv_kernel<NT, EPI_ADD><<<grid, kGemvThreads, 0, st>>>(p); break;
+    case EPI_GATEUP: stream_gemv_kernel<NT, EPI_GATEUP><<<grid, kGemvThreads, 0, st>>>(p); break;
+    case EPI_DOWN: stream_gemv_kernel<NT, EPI_DOWN><<<grid, kGemvThreads, 0, st>>>(p); break;
+    case EPI_ARGMAX: stream_gemv_kernel<NT, EPI_ARGMAX><<<grid, kGemvThreads, 0, st>>>(p); break;
+    }
+}
+static void launch_gemv(int epi, const GemvParams& p, int grid, cudaStream_t st) {
+    if (p.T <= 8) launch_gemv_nt<1>(epi, p, grid, st);
+    else launch_gemv_nt<2>(epi, p, grid, st);
+}
+
+static GemvParams gemv_base(cascade_session* s, int T) {
+    GemvParams p{};
+    p.T = T;
+    p.min_seg = 8;
+    p.partial = s->partial;
+    p.counters = s->counters;
+    p.n_blocks = 1;
+    return p;
+}
+
+// Optional per-launch event pairs (cascade_profile_step).
+struct Prof {
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> kind;
+    cudaStream_t st = nullptr;
+    void begin(int k) {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+        ev.push_back(a);
+        ev.push_back(b);
+        kind.push_back(k);
+    }
+    void end() { cudaEventRecord(ev.back(), st); }
+    ~Prof() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+#define PB(k) \
+    if (prof) prof->begin(k)
+#define PE() \
+    if (prof) prof->end()
+
+// Enqueues one full step of width T on s->stream; returns the number of
+// kernels launched through *n_kernels.
+static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = nullptr) {
+    cascade_model* m = s->m;
+    const Dims D(m->g);
+    const cudaStream_t st = s->stream;
+    const bool taps = s->taps_on;
+    int nk = 0;
+    CK(cudaMemcpyAsync(s->d_params, s->h_params, sizeof(StepParams), cudaMemcpyHostToDevice, st));
+
+    EmbedParams ep{};
+    ep.sp = s->d_params;
+    ep.st = s->d_state;
+    ep.embed = m->embed;
+    ep.norm_w = m->layers[0].attn_norm;
+    ep.x = s->x;
+    ep.xn_bfrag = s->xn;
+    ep.tokens_used = s->tokens_used;
+    ep.stamp = s->stamps;
+    ep.tap_x = taps ? s->taps.x_in : nullptr;
+    ep.tap_xn = taps ? s->taps.xn_attn : nullptr;
+    ep.T = T;
+    ep.d = D.d;
+    ep.eps = m->g.norm_eps;
+    PB(0);
+    embed_norm_kernel<<<T, kRouteThreads, 0, st>>>(ep);
+    PE();
+    ++nk;
+
+    const int G = D.H / D.KV;
+    for (int l = 0; l < D.L; ++l) {
+        const LayerW& w = m->layers[l];
+        const size_t td = (size_t)l * kMaxT * D.d;
+        // QKV
+        GemvParams q = gemv_base(s, T);
+        q.W = w.wqkv;
+        q.B = reinterpret_cast<const uint2*>(s->xn);
+        q.n_st = D.qkvd / kSTRows;
+        q.n_ks = D.d / 16;
+        q.out = s->qkv;
+        q.ld = D.qkvd;
+        q.stamp = s->stamps + 1 + 2 * l;
+        PB(1);
+        launch_gemv(EPI_STORE, q, s->gemv_grid, st);
+        PE();
+        ++nk;
+        // attention
+        AttnParams ap{};
+        ap.qkv = s->qkv;
+        ap.kc = s->kc + (size_t)l * D.KV * s->max_ctx * D.hd;
+        ap.vc = s->vc + (size_t)l * D.KV * s->max_ctx * D.hd;
+        ap.ctx_ptr = &s->d_state->cache_len;
+        ap.part = s->attn_part;
+        ap.T = T;
+        ap.H = D.H;
+        ap.KV = D.KV;
+        ap.max_ctx = s->max_ctx;
+        ap.max_chunks = s->max_chunks;
+        ap.rope_theta = (double)m->g.rope_theta;
+        ap.scale = 1.0f / sqrtf((float)D.hd);
+        const int agrid = m->num_sms;
+        PB(2);
+        if (D.hd == 32) attn_partial_kernel<32><<<agrid, kAttnThreads, attn_smem_bytes<32>(), st>>>(ap);
+        else if (D.hd == 64) attn_partial_kernel<64><<<agrid, kAttnThreads, attn_smem_bytes<64>(), st>>>(ap);
+        else attn_partial_kernel<128><<<agrid, kAttnThreads, attn_smem_bytes<128>(), st>>>(ap);
+        PE();
+        ++nk;
+        AttnCombineParams cp{};
+        cp.part = s->attn_part;
+        cp.ctx_ptr = &s->d_state->cache_len;
+        cp.out_bfrag = s->attn_out;
+        cp.tap = nullptr;
+        cp.T = T;
+        cp.H = D.H;
+        cp.KV = D.KV;
+        cp.hd = D.hd;
+        cp.max_chunks = s->max_chunks;
+        PB(3);
+        attn_combine_kernel<<<dim3(T, D.H), D.hd, 0, st>>>(cp);
+        PE();
+        ++nk;
+        (void)G;
+        // O projection + residual
+        GemvParams o = gemv_base(s, T);
+        o.W = w.wo;
+        o.B = reinterpret_cast<const uint2*>(s->attn_out);
+        o.n_st = D.d / kSTRows;
+        o.n_ks = D.hq / 16;
+        o.out = s->x;
+        o.ld = D.d;
+        PB(4);
+        launch_gemv(EPI_ADD, o, s->gemv_grid, st);
+        PE();
+        ++nk;
+        if (taps) CK(cudaMemcpyAsync(s->taps.x_mid + td, s->x, (size_t)T * D.d * 4, cudaMemcpyDeviceToDevice, st));
+        // route: norm + router + top-k + union
+        RouteParams rp{};
+        rp.x = s->x;
+        rp.norm_w = w.ffn_norm;
+        rp.router_w = w.router;
+        rp.xn_bfrag = s->xn;
+        rp.logits = s->logits_router;
+        rp.ticket = s->ticket;
+        rp.topk_id = s->topk_id;
+        rp.topk_w = s->topk_w;
+        rp.gsh = s->gsh;
+        rp.list = s->list;
+        rp.count = s->count;
+        rp.route_rank = s->route_rank;
+        rp.union_size = s->union_size + l;
+        rp.ycontrib = s->ycontrib;
+        rp.tap_xn = taps ? s->taps.xn_moe + td : nullptr;
+        rp.T = T;
+        rp.d = D.d;
+        rp.E = D.E;
+        rp.k = D.k;
+        rp.S = D.S;
+        rp.renorm = m->g.renormalize_topk;
+        rp.shared_gate = m->g.shared_gate;
+        rp.e_lo = m->e_lo;
+        rp.e_hi = m->e_hi;
+        rp.ep_rank = m->ep_rank;
+        rp.ep_size = m->ep_size;
+        rp.eps = m->g.norm_eps;
+        rp.zero_nonlocal = m->ep_size > 1;
+        rp.stamp = s->stamps + 2 + 2 * l;
+        PB(5);
+        moe_route_kernel<<<T, kRouteThreads, D.d * 4, st>>>(rp);
+        PE();
+        ++nk;
+        if (taps) {
+            CK(cudaMemcpyAsync(s->taps.logits + (size_t)l * kMaxT * (D.E + 1), s->logits_router,
+                               (size_t)T * (D.E + 1) * 4, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(s->taps.topk_id + (size_t)l * kMaxT * D.k, s->topk_id, (size_t)T * D.k * 4,
+                               cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(s->taps.topk_w + (size_t)l * kMaxT * D.k, s->topk_w, (size_t)T * D.k * 4,
+                               cudaMemcpyDeviceToDevice, st));
+        }
+        // experts: gate/up (+SiLU) then down, over the active list only
+        GemvParams gu = gemv_base(s, T);
+        gu.W = w.w13;
+        gu.w_block_stride = D.w13_vec;
+        gu.B = reinterpret_cast<const uint2*>(s->xn);
+        gu.b_block_stride = 0;
+        gu.list = s->list;
+        gu.count = s->count;
+        gu.n_st = 2 * D.f / kSTRows;
+        gu.n_ks = D.d / 16;
+        gu.hout = s->hbuf;
+        gu.h_block_stride = (long long)D.f * 16;
+        PB(6);
+        launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st);
+        PE();
+        ++nk;
+        GemvParams dn = gemv_base(s, T);
+        dn.W = w.w2;
+        dn.w_block_stride = D.w2_vec;
+        dn.B = reinterpret_cast<const uint2*>(s->hbuf);
+        dn.b_block_stride = (long long)D.f * 4;  // uint2 units per slot
+        dn.list = s->list;
+        dn.count = s->count;
+        dn.n_st = D.d / kSTRows;
+        dn.n_ks = D.f / 16;
+        dn.route_rank = s->route_rank;
+        dn.n_contrib = D.k + D.S;
+        dn.out = s->ycontrib;
+        dn.ld = D.d;
+        PB(7);
+        launch_gemv(EPI_DOWN, dn, s->gemv_grid, st);
+        PE();
+        ++nk;
+        if (m->ep_size > 1) {
+            PB(11);
+            const int nr = g_nccl.AllReduce(s->ycontrib, s->ycontrib, (size_t)T * (D.k + D.S) * D.d, kNcclFloat32,
+                                            kNcclSum, m->comm, st);
+            PE();
+            if (nr != 0) return set_err(CASCADE_ERUNTIME, "ncclAllReduce failed");
+        }
+        CombineParams c{};
+        c.x = s->x;
+        c.ycontrib = s->ycontrib;
+        c.topk_w = s->topk_w;
+        c.gsh = s->gsh;
+        c.norm_w = (l + 1 < D.L) ? m->layers[l + 1].attn_norm : m->final_norm;
+        c.xn_bfrag = s->xn;
+        c.tap_moe = taps ? s->taps.moe_out + td : nullptr;
+        c.tap_xn = (taps && l + 1 < D.L) ? s->taps.xn_attn + td + (size_t)kMaxT * D.d : nullptr;
+        c.tap_x = (taps && l + 1 < D.L) ? s->taps.x_in + td + (size_t)kMaxT * D.d : nullptr;
+        c.T = T;
+        c.d = D.d;
+        c.k = D.k;
+        c.S = D.S;
+        c.eps = m->g.norm_eps;
+        PB(8);
+        moe_combine_kernel<<<T, kRouteThreads, 0, st>>>(c);
+        PE();
+        ++nk;
+    }
+    // LM head + argmax
+    GemvParams lm = gemv_base(s, T);
+    lm.W = m->lm_head;
+    lm.B = reinterpret_cast<const uint2*>(s->xn);
+    lm.n_st = D.V / kSTRows;
+    lm.n_ks = D.d / 16;
+    lm.keys = s->keys;
+    lm.out = taps ? s->taps.final_logits : nullptr;
+    lm.ld = D.V;
+    lm.stamp = s->stamps + 1 + 2 * D.L;
+    PB(9);
+    launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st);
+    PE();
+    ++nk;
+    AcceptParams ap{};
+    ap.sp = s->d_params;
+    ap.st = s->d_state;
+    ap.keys = s->keys;
+    ap.tokens_used = s->tokens_used;
+    ap.stamps = s->stamps;
+    ap.union_size = s->union_size;
+    ap.res = s->d_result;
+    ap.T = T;
+    ap.L = D.L;
+    ap.S = D.S;
+    PB(10);
+    accept_kernel<<<1, 32, 0, st>>>(ap);
+    PE();
+    ++nk;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s->h_result, s->d_result, sizeof(cascade_verify_out), cudaMemcpyDeviceToHost, st));
+    if (n_kernels) *n_kernels = nk;
+    return CASCADE_OK;
+}
+
+static int ensure_graph(cascade_session* s, int T) {
+    if (s->graph[T]) return CASCADE_OK;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    int nk = 0;
+    int rc = enqueue_step(s, T, &nk);
+    cudaError_t e = cudaStreamEndCapture(s->stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return set_err(CASCADE_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&s->graph[T], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return set_err(CASCADE_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    s->graph_kernels[T] = nk;
+    return CASCADE_OK;
+}
+
+static int run_step(cascade_session* s, int T) {
+    if (s->taps_on) return enqueue_step(s, T, nullptr);
+    int rc = ensure_graph(s, T);
+    if (rc) return rc;
+    CK(cudaGraphLaunch(s->graph[T], s->stream));
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_profile_step(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n) {
+    if (!s || !ns || !kind || !n || K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "bad arguments");
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    const int T = K + 1;
+    s->h_params->mode = 0;
+    s->h_params->commit = 0;
+    s->h_params->T = T;
+    s->h_params->t_base_ns = s->t_base_ns;
+    Prof prof;
+    prof.st = s->stream;
+    int rc = enqueue_step(s, T, nullptr, &prof);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s->stream));
+    const int cnt = (int)prof.kind.size();
+    if (cnt > cap) return set_err(CASCADE_EINVAL, "profile buffer too small: need " + std::to_string(cnt));
+    for (int i = 0; i < cnt; ++i) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, prof.ev[2 * i], prof.ev[2 * i + 1]));
+        ns[i] = (double)ms * 1.0e6;
+        kind[i] = prof.kind[i];
+    }
+    *n = cnt;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_step_kernel_count(cascade_session* s, int K, int* out) {
+    if (!s || !out || K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "bad arguments");
+    CK(cudaSetDevice(s->m->device));
+    int rc = ensure_graph(s, K + 1);
+    if (rc) return rc;
+    *out = s->graph_kernels[K + 1];
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_session_reset(cascade_session* s) {
+    if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemset(s->d_state, 0, sizeof(DevState)));
+    CK(cudaDeviceSynchronize());
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_set_baseline(cascade_session* s, double t_base_ns) {
+    if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
+    if (!(t_base_ns > 0.0)) return set_err(CASCADE_EINVAL, "set_baseline: t_base must be > 0");
+    s->t_base_ns = t_base_ns;
+    return CASCADE_OK;
+}
+
+static int read_state(cascade_session* s, DevState* out) {
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(out, s->d_state, sizeof(DevState), cudaMemcpyDeviceToHost));
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_prefill(cascade_session* s, const int32_t* prompt, int n) {
+    if (!s || !prompt) return set_err(CASCADE_EINVAL, "session/prompt is NULL");
+    if (n < 1) return set_err(CASCADE_EINVAL, "prefill: need at least one token");
+    CK(cudaSetDevice(s->m->device));
+    DevState ds;
+    int rc = read_state(s, &ds);
+    if (rc) return rc;
+    if (ds.cache_len + n - 1 + kMaxT > s->max_ctx) return set_err(CASCADE_EINVAL, "prefill exceeds max_ctx");
+    for (int i = 0; i < n; ++i)
+        if (prompt[i] < 0 || prompt[i] >= s->m->g.vocab) return set_err(CASCADE_EINVAL, "token id out of range");
+    int pos = 0;
+    while (pos < n - 1) {
+        const int T = std::min(kMaxT, n - 1 - pos);
+        CK(cudaStreamSynchronize(s->stream));
+        std::memset(s->h_params, 0, sizeof(StepParams));
+        s->h_params->mode = 1;
+        s->h_params->commit = 1;
+        s->h_params->T = T;
+        for (int i = 0; i < T; ++i) s->h_params->tokens[i] = prompt[pos + i];
+        if ((rc = run_step(s, T))) return rc;
+        pos += T;
+    }
+    CK(cudaStreamSynchronize(s->stream));
+    const int32_t last = prompt[n - 1];
+    CK(cudaMemcpy(&s->d_state->pending, &last, 4, cudaMemcpyHostToDevice));
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_verify(cascade_session* s, const int32_t* draft, int K, double draft_ns,
+                              cascade_verify_out* out) {
+    if (!s || !out) return set_err(CASCADE_EINVAL, "session/out is NULL");
+    if (K < 0 || K > s->k_max) return set_err(CASCADE_EINVAL, "verify: K must be in [0, k_max]");
+    if (K > 0 && !draft) return set_err(CASCADE_EINVAL, "verify: draft is NULL");
+    for (int i = 0; i < K; ++i)
+        if (draft[i] < 0 || draft[i] >= s->m->g.vocab) return set_err(CASCADE_EINVAL, "draft token out of range");
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    const int T = K + 1;
+    std::memset(s->h_params, 0, sizeof(StepParams));
+    s->h_params->mode = 0;
+    s->h_params->commit = 1;
+    s->h_params->T = T;
+    for (int i = 0; i < K; ++i) s->h_params->tokens[i + 1] = draft[i];
+    s->h_params->t_base_ns = s->t_base_ns;
+    s->h_params->draft_ns = draft_ns;
+    int rc = run_step(s, T);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s->stream));
+    *out = *s->h_result;
+    if (out->cache_len + kMaxT > s->max_ctx) {
+        // the next step would not fit; report it now (the caller owns policy)
+        return set_err(CASCADE_ERUNTIME, "session KV cache is full (max_ctx reached)");
+    }
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_verify_enqueue(cascade_session* s, int K, int commit) {
+    if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
+    if (K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "K out of range");
+    const int T = K + 1;
+    s->h_params->mode = 0;
+    s->h_params->commit = commit ? 1 : 0;
+    s->h_params->T = T;
+    s->h_params->t_base_ns = s->t_base_ns;
+    int rc = run_step(s, T);
+    return rc;
+}
+
+extern "C" int cascade_sync(cascade_session* s) {
+    if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
+    CK(cudaStreamSynchronize(s->stream));
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_last_union_sizes(cascade_session* s, int32_t* out, int n) {
+    if (!s || !out || n < s->m->g.num_layers) return set_err(CASCADE_EINVAL, "need num_layers ints");
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(out, s->union_size, (size_t)s->m->g.num_layers * 4, cudaMemcpyDeviceToHost));
+    return CASCADE_OK;
+}
+
+// ---------------------------------------------------------------- taps
+extern "C" int cascade_enable_taps(cascade_session* s, int enable) {
+    if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
+    const Dims D(s->m->g);
+    if (enable && !s->taps.x_in) {
+        const size_t ld = (size_t)D.L * kMaxT;
+        int rc;
+        if ((rc = salloc(s, &s->taps.xn_moe, ld * D.d * 2)) || (rc = salloc(s, &s->taps.logits, ld * (D.E + 1) * 4)) ||
+            (rc = salloc(s, &s->taps.topk_id, ld * D.k * 4)) || (rc = salloc(s, &s->taps.topk_w, ld * D.k * 4)) ||
+            (rc = salloc(s, &s->taps.moe_out, ld * D.d * 4)) ||
+            (rc = salloc(s, &s->taps.final_logits, (size_t)kMaxT * D.V * 4)) ||
+            (rc = salloc(s, &s->taps.xn_attn, ld * D.d * 2)) || (rc = salloc(s, &s->taps.x_mid, ld * D.d * 4)) ||
+            (rc = salloc(s, &s->taps.x_in, ld * D.d * 4)))
+            return rc;
+    }
+    s->taps_on = enable != 0;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_read_tap(cascade_session* s, int kind, void* out, size_t bytes) {
+    if (!s || !out) return set_err(CASCADE_EINVAL, "session/out is NULL");
+    if (!s->taps.x_in) return set_err(CASCADE_EINVAL, "taps are not enabled");
+    const Dims D(s->m->g);
+    const size_t ld = (size_t)D.L * kMaxT;
+    const void* src = nullptr;
+    size_t n = 0;
+    switch (kind) {
+    case 0: src = s->taps.xn_moe; n = ld * D.d * 2; break;
+    case 1: src = s->taps.logits; n = ld * (D.E + 1) * 4; break;
+    case 2: src = s->taps.topk_id; n = ld * D.k * 4; break;
+    case 3: src = s->taps.topk_w; n = ld * D.k * 4; break;
+    case 4: src = s->taps.moe_out; n = ld * D.d * 4; break;
+    case 5: src = s->taps.final_logits; n = (size_t)kMaxT * D.V * 4; break;
+    case 6: src = s->taps.xn_attn; n = ld * D.d * 2; break;
+    case 7: src = s->taps.x_mid; n = ld * D.d * 4; break;
+    case 8: src = s->taps.x_in; n = ld * D.d * 4; break;
+    default: return set_err(CASCADE_EINVAL, "unknown tap kind");
+    }
+    if (bytes != n) return set_err(CASCADE_EINVAL, "tap size mismatch: expected " + std::to_string(n));
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    CK(cudaMemcpy(out, src, n, cudaMemcpyDeviceToHost));
+    return CASCADE_OK;
+}
+
+// ---------------------------------------------------------------- weights readback
+__global__ void afrag_extract_kernel(const uint16_t* src, int n_ks, int row_phys0, int phys_step_mode, int nrows,
+                                     int cols, uint16_t* dst) {
+    // phys_step_mode: 0 = rows contiguous; 1 = gate rows; 2 = up rows (GATEUP layout)
+    const long long n = (long long)nrows * cols;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int rr = (int)(i / cols), c = (int)(i % cols);
+        int R;
+        if (phys_step_mode == 0) R = row_phys0 + rr;
+        else {
+            const int j = row_phys0 + rr;
+            R = (j / 8) * 16 + (phys_step_mode == 2 ? 8 : 0) + (j % 8);
+        }
+        const int st = R / kSTRows, it = (R % kSTRows) / 16, r = R % 16;
+        const int s = c / 16, cc = c % 16;
+        const int g = r % 8, t = (cc % 8) / 2;
+        const int e = (cc / 8) * 4 + (r / 8) * 2 + (cc % 2);
+        const int lane = g * 4 + t;
+        dst[i] = src[((((long long)st * n_ks + s) * kTPW + it) * 32 + lane) * 8 + e];
+    }
+}
+
+extern "C" int cascade_read_weight(cascade_model* m, int kind, int layer, int expert, int row0, int nrows,
+                                   uint16_t* out) {
+    if (!m || !out || nrows < 1 || row0 < 0) return set_err(CASCADE_EINVAL, "bad arguments");
+    const Dims D(m->g);
+    if ((kind != CASCADE_T_EMBED && kind != CASCADE_T_LM_HEAD && kind != CASCADE_T_FINAL_NORM) &&
+        (layer < 0 || layer >= D.L))
+        return set_err(CASCADE_EINVAL, "layer out of range");
+    CK(cudaSetDevice(m->device));
+    const uint16_t* plain = nullptr;
+    int cols = D.d, rows_total = 0;
+    const uint4* af = nullptr;
+    int n_ks = 0, mode = 0, phys0 = row0;
+    switch (kind) {
+    case CASCADE_T_EMBED: plain = m->embed; rows_total = D.V; break;
+    case CASCADE_T_FINAL_NORM: plain = m->final_norm; rows_total = 1; break;
+    case CASCADE_T_ATTN_NORM: plain = m->layers[layer].attn_norm; rows_total = 1; break;
+    case CASCADE_T_FFN_NORM: plain = m->layers[layer].ffn_norm; rows_total = 1; break;
+    case CASCADE_T_ROUTER: plain = m->layers[layer].router; rows_total = D.E; break;
+    case CASCADE_T_SHARED_GATE:
+        plain = m->layers[layer].router + (size_t)D.E * D.d; rows_total = m->g.shared_gate ? 1 : 0; break;
+    case CASCADE_T_WQ: af = m->layers[layer].wqkv; rows_total = D.hq; n_ks = D.d / 16; break;
+    case CASCADE_T_WK: af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + row0; break;
+    case CASCADE_T_WV:
+        af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + D.KV * D.hd + row0; break;
+    case CASCADE_T_WO: af = m->layers[layer].wo; rows_total = D.d; cols = D.hq; n_ks = D.hq / 16; break;
+    case CASCADE_T_LM_HEAD: af = m->lm_head; rows_total = D.V; n_ks = D.d / 16; break;
+    case CASCADE_T_W_GATE:
+    case CASCADE_T_W_UP:
+    case CASCADE_T_W_DOWN: {
+        int b = -1;
+        if (expert >= m->e_lo && expert < m->e_hi) b = expert - m->e_lo;
+        else if (expert >= D.E && expert < D.E + D.S && ((expert - D.E) % m->ep_size) == m->ep_rank) {
+            int lb = 0;
+            for (int s2 = 0; s2 < expert - D.E; ++s2) lb += (s2 % m->ep_size) == m->ep_rank;
+            b = (m->e_hi - m->e_lo) + lb;
+        }
+        if (b < 0) return set_err(CASCADE_EINVAL, "expert is not held by this rank");
+        if (kind == CASCADE_T_W_DOWN) {
+            af = m->layers[layer].w2 + (size_t)b * D.w2_vec; rows_total = D.d; cols = D.f; n_ks = D.f / 16;
+        } else {
+            af = m->layers[layer].w13 + (size_t)b * D.w13_vec; rows_total = D.f; n_ks = D.d / 16;
+            mode = kind == CASCADE_T_W_GATE ? 1 : 2;
+        }
+        break;
+    }
+    default: return set_err(CASCADE_EINVAL, "unknown tensor kind");
+    }
+    if (row0 + nrows > rows_total) return set_err(CASCADE_EINVAL, "rows out of range");
+    const size_t n = (size_t)nrows * cols;
+    if (plain) {
+        CK(cudaMemcpy(out, plain + (size_t)row0 * cols, n * 2, cudaMemcpyDeviceToHost));
+        return CASCADE_OK;
+    }
+    uint16_t* tmp = nullptr;
+    CK(cudaMalloc(&tmp, n * 2));
+    afrag_extract_kernel<<<256, 256>>>(reinterpret_cast<const uint16_t*>(af), n_ks, phys0, mode, nrows, cols, tmp);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(out, tmp, n * 2, cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    if (e != cudaSuccess) return set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_read_kv(cascade_session* s, int layer, int which, int len, uint16_t* out) {
+    if (!s || !out || layer < 0 || layer >= s->m->g.num_layers || len < 0 || len > s->max_ctx)
+        return set_err(CASCADE_EINVAL, "bad arguments");
+    const Dims D(s->m->g);
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    const uint16_t* base = (which ? s->vc : s->kc) + (size_t)layer * D.KV * s->max_ctx * D.hd;
+    for (int h = 0; h < D.KV; ++h)
+        CK(cudaMemcpy(out + (size_t)h * len * D.hd, base + (size_t)h * s->max_ctx * D.hd, (size_t)len * D.hd * 2,
+                      cudaMemcpyDeviceToHost));
+    return CASCADE_OK;
+}

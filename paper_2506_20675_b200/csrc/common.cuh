@@ -1,0 +1,130 @@
+// common.cuh — device helpers shared by every kernel of the verify step.
+//
+// Data layouts in HBM:
+//  * A-frag (weights).  A [rows, K] matrix is cut into super-tiles of
+//    kTPW*16 = 64 rows; each super-tile is stored k-step by k-step (16
+//    columns), and inside a k-step the kTPW 16x16 tiles are stored as the 32
+//    lanes' mma.m16n8k16 A-fragments: lane (g = lane/4, t = lane%4) owns the
+//    16 bytes {W[g][2t..2t+1], W[g+8][2t..2t+1], W[g][2t+8..2t+9],
+//    W[g+8][2t+8..2t+9]}.  One warp therefore streams a weight matrix with
+//    one fully coalesced 512-byte LDG.128 per tile per k-step and the bytes
+//    land directly in mma registers: no shared-memory transpose, no bank
+//    conflicts, no per-element index math on the hot path.
+//  * B-frag (activations, <= 16 tokens).  Element (tok, k) of a [16, K]
+//    bf16 activation lives where lane (g = tok%8, t = (k%8)/2) of n-tile
+//    tok/8 expects it for k-step k/16: one 8-byte LDG.64 per n-tile per
+//    k-step.  Producers (norms, SiLU epilogue, attention) write this layout
+//    directly.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cascade_weights.h"
+
+namespace cascade {
+
+constexpr int kTPW = 4;                 // 16-row tiles per super-tile (per warp)
+constexpr int kSTRows = 16 * kTPW;      // 64 rows per super-tile
+constexpr int kMaxT = 16;               // tokens in flight (two n8 tiles)
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Weights are read exactly once per step: bypass L1, keep them from
+// displacing activations in L2 (evict_first).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile(
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
+
+// Activations: small, re-read by every warp of the SM -> cache in L1.
+__device__ __forceinline__ uint2 ldg_act(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint4& a, const uint2& b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "
+        "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y));
+}
+
+// bf16 element index of activation (tok, k) inside a B-frag buffer.
+__host__ __device__ __forceinline__ long long bfrag_index(int tok, int k) {
+    const int s = k >> 4, kk = k & 15;
+    const int hi = kk >> 3, kk2 = kk & 7;
+    const int t = kk2 >> 1, w = kk2 & 1;
+    const int nt = tok >> 3, g = tok & 7;
+    const int lane = g * 4 + t;
+    return ((((long long)s * 2 + nt) * 32 + lane) * 4) + hi * 2 + w;
+}
+
+// Logical (row, col) of bf16 element `e` (0..7) of lane `lane` in a 16x16 tile.
+__host__ __device__ __forceinline__ void afrag_coords(int lane, int e, int& r, int& c) {
+    const int g = lane >> 2, t = lane & 3;
+    r = g + 8 * ((e >> 1) & 1);
+    c = 2 * t + (e & 1) + 8 * (e >> 2);
+}
+
+__device__ __forceinline__ float bf16_round(float x) {
+    return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ uint16_t bf16_bits(float x) {
+    __nv_bfloat16 h = __float2bfloat16_rn(x);
+    return *reinterpret_cast<uint16_t*>(&h);
+}
+
+__device__ __forceinline__ float bits_to_f32(uint16_t b) {
+    return __uint_as_float(((uint32_t)b) << 16);
+}
+
+// Block-wide sum (blockDim.x multiple of 32, <= 1024). `red` holds 32 floats.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    float s = 0.f;
+    if (warp == 0) {
+        s = lane < nw ? red[lane] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[0] = s;
+    }
+    __syncthreads();
+    s = red[0];
+    __syncthreads();
+    return s;
+}
+
+// Order-preserving float key for atomicMax argmax; low word breaks ties
+// toward the lower index (reference tie rule, controller.hpp:124-125).
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+    uint32_t u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)u << 32) | (0xFFFFFFFFu - (uint32_t)idx);
+}
+__device__ __forceinline__ int argmax_key_index(unsigned long long k) {
+    return (int)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+
+}  // namespace cascade

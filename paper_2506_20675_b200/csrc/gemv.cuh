@@ -1,0 +1,283 @@
+// gemv.cuh — the weight-streaming engine behind every linear layer of the
+// verify step (QKV, O, routed + shared expert gate/up and down, LM head).
+//
+// Problem shape: Y[T, rows] = X[T, K] * W[rows, K]^T with T = K_spec+1 <= 16
+// tokens, i.e. a batch of GEMVs whose cost is the weight bytes (arithmetic
+// intensity T flop/B, far below the tensor-core ridge).  The design goal is
+// to stream each *active* weight block from HBM exactly once at copy speed:
+//
+//  * Work = (active block, 64-row super-tile, 16-column k-step).  The flat
+//    work range U*n_st*n_ks is split into one contiguous, equal-length range
+//    per warp (stream-K), so every SM moves the same number of bytes no
+//    matter how many experts the router activated (U is read from device
+//    memory: the same captured graph serves every routing outcome).
+//  * Each k-step a warp issues kTPW LDG.128 of A-fragments (512 B each, see
+//    common.cuh) and one LDG.64 per n8 token tile, then kTPW*NT
+//    mma.sync.m16n8k16 (fp32 accumulate).  kUnroll k-steps are loaded
+//    before any math so ~8 KB per warp is in flight.
+//  * A super-tile split between warps is finished by the last-arriving
+//    warp, which sums the partials in worker order: deterministic for a
+//    given (U, grid), no float atomics.
+//  * The epilogue is fused: plain store, residual add, SiLU(gate)*up into
+//    the next GEMV's B-frag layout, scatter into the expert-combine buffer,
+//    or the LM-head argmax.
+#pragma once
+
+#include "common.cuh"
+
+namespace cascade {
+
+enum Epi : int {
+    EPI_STORE = 0,   // out[tok*ld + row] = v
+    EPI_ADD = 1,     // out[tok*ld + row] += v      (residual)
+    EPI_GATEUP = 2,  // H[slot] (B-frag, bf16) = silu(gate) * up
+    EPI_DOWN = 3,    // ycontrib[(tok*n_contrib + rank)*ld + row] = v
+    EPI_ARGMAX = 4,  // keys[tok] = max(argmax_key(v, row)); optional logits store
+};
+
+struct GemvParams {
+    const uint4* W;            // A-frag weights of local block 0
+    long long w_block_stride;  // uint4 units between blocks
+    const uint2* B;            // B-frag activations (list slot 0)
+    long long b_block_stride;  // uint2 units between list slots (0: shared X)
+    const int* list;           // active block ids, or nullptr (identity)
+    const int* count;          // device U, or nullptr (use n_blocks)
+    int n_blocks;
+    int n_st;                  // super-tiles per block
+    int n_ks;                  // k-steps per block (K / 16)
+    int T;                     // tokens in flight
+    int min_seg;               // minimum k-steps per worker
+    float4* partial;           // stream-K partials [workers][2][kTPW][NT][32]
+    int* counters;             // per-unit arrival counters (zero between launches)
+    float* out;                // EPI_STORE / EPI_ADD / EPI_DOWN / EPI_ARGMAX (opt.)
+    int ld;                    // leading dimension of out
+    uint16_t* hout;            // EPI_GATEUP output (B-frag bf16)
+    long long h_block_stride;  // bf16 units between list slots
+    const int* route_rank;     // EPI_DOWN: [slot][16] -> rank in token's list or -1
+    int n_contrib;             // EPI_DOWN
+    unsigned long long* keys;  // EPI_ARGMAX
+    unsigned long long* stamp; // optional globaltimer stamp at kernel start
+};
+
+constexpr int kGemvThreads = 256;
+constexpr int kGemvWarps = kGemvThreads / 32;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int NT, int EPI>
+__device__ __forceinline__ void gemv_epilogue(const GemvParams& p, int bl, int st, int lane,
+                                              float (&acc)[kTPW][NT][4]) {
+    const int g = lane >> 2, t = lane & 3;
+    if constexpr (EPI == EPI_STORE || EPI == EPI_ADD) {
+#pragma unroll
+        for (int it = 0; it < kTPW; ++it) {
+            const int row = st * kSTRows + it * 16 + g;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const int tok = nt * 8 + 2 * t;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int tk = tok + (c & 1);
+                    const int r = row + 8 * (c >> 1);
+                    if (tk < p.T) {
+                        float* o = p.out + (long long)tk * p.ld + r;
+                        if constexpr (EPI == EPI_ADD) *o += acc[it][nt][c];
+                        else *o = acc[it][nt][c];
+                    }
+                }
+            }
+        }
+    } else if constexpr (EPI == EPI_GATEUP) {
+        // rows g (gate j) and g+8 (up j) of each tile share j.
+        uint16_t* H = p.hout + (long long)bl * p.h_block_stride;
+#pragma unroll
+        for (int it = 0; it < kTPW; ++it) {
+            const int j = st * (kSTRows / 2) + it * 8 + g;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int tk = nt * 8 + 2 * t + c;
+                    const float gate = acc[it][nt][c];
+                    const float up = acc[it][nt][2 + c];
+                    const float h = tk < p.T ? silu(gate) * up : 0.0f;
+                    H[bfrag_index(tk, j)] = bf16_bits(h);
+                }
+            }
+        }
+    } else if constexpr (EPI == EPI_DOWN) {
+        const int* rr = p.route_rank + bl * kMaxT;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int tk = nt * 8 + 2 * t + c;
+                if (tk >= p.T) continue;
+                const int rank = rr[tk];
+                if (rank < 0) continue;
+                float* o = p.out + ((long long)tk * p.n_contrib + rank) * p.ld;
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it) {
+                    const int row = st * kSTRows + it * 16 + g;
+                    o[row] = acc[it][nt][c];
+                    o[row + 8] = acc[it][nt][2 + c];
+                }
+            }
+        }
+    } else if constexpr (EPI == EPI_ARGMAX) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int tk = nt * 8 + 2 * t + c;
+                unsigned long long best = 0ull;
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it) {
+                    const int row = st * kSTRows + it * 16 + g;
+                    const unsigned long long k0 = argmax_key(acc[it][nt][c], row);
+                    const unsigned long long k1 = argmax_key(acc[it][nt][2 + c], row + 8);
+                    best = k0 > best ? k0 : best;
+                    best = k1 > best ? k1 : best;
+                    if (p.out != nullptr && tk < p.T) {
+                        p.out[(long long)tk * p.ld + row] = acc[it][nt][c];
+                        p.out[(long long)tk * p.ld + row + 8] = acc[it][nt][2 + c];
+                    }
+                }
+                // reduce over the 8 lanes (g) that hold the same token
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+                    best = other > best ? other : best;
+                }
+                if (g == 0 && tk < p.T) atomicMax(p.keys + tk, best);
+            }
+        }
+    }
+}
+
+// worker containing flat position q when [0,total) is split into n ranges
+// [floor(total*w/n), floor(total*(w+1)/n))
+__device__ __forceinline__ int worker_of(long long q, long long total, int n) {
+    return (int)(((q + 1) * n + total - 1) / total) - 1;
+}
+
+template <int NT, int EPI>
+__global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams p) {
+    if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
+    const int lane = threadIdx.x & 31;
+    const int U = p.count ? *p.count : p.n_blocks;
+    const long long per_block = (long long)p.n_st * p.n_ks;
+    const long long total = (long long)U * per_block;
+    if (total <= 0) return;
+    long long nmax = total / p.min_seg;
+    if (nmax < 1) nmax = 1;
+    int N = gridDim.x * kGemvWarps;
+    if (N > nmax) N = (int)nmax;
+    const int w = blockIdx.x * kGemvWarps + (threadIdx.x >> 5);
+    if (w >= N) return;
+    const long long lo = total * w / N;
+    const long long hi = total * (w + 1) / N;
+
+    const uint64_t pol = policy_evict_first();
+    long long pos = lo;
+    while (pos < hi) {
+        const long long unit = pos / p.n_ks;
+        const int ks0 = (int)(pos - unit * p.n_ks);
+        const long long rem = hi - pos;
+        const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
+        const int bl = (int)(unit / p.n_st);
+        const int st = (int)(unit - (long long)bl * p.n_st);
+        const int blk = p.list ? p.list[bl] : bl;
+        const uint4* A = p.W + (long long)blk * p.w_block_stride +
+                         (long long)st * p.n_ks * (kTPW * 32) + lane;
+        const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
+
+        float acc[kTPW][NT][4];
+#pragma unroll
+        for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[it][nt][c] = 0.f;
+
+        int s = ks0;
+        for (; s + kUnroll <= ks1; s += kUnroll) {
+            uint4 a[kUnroll][kTPW];
+            uint2 b[kUnroll][NT];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it)
+                    a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) b[u][nt] = ldg_act(Bp + ((s + u) * 2 + nt) * 32);
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], b[u][nt]);
+        }
+        for (; s < ks1; ++s) {
+            uint4 a[kTPW];
+            uint2 b[NT];
+#pragma unroll
+            for (int it = 0; it < kTPW; ++it) a[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) b[nt] = ldg_act(Bp + (s * 2 + nt) * 32);
+#pragma unroll
+            for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[it], b[nt]);
+        }
+        pos += ks1 - ks0;
+
+        if (!(ks0 == 0 && ks1 == p.n_ks)) {
+            // split super-tile: publish the partial, last arriver reduces
+            const long long ustart = unit * p.n_ks;
+            const int first = worker_of(ustart, total, N);
+            const int last = worker_of(ustart + p.n_ks - 1, total, N);
+            const int slot = (w == first) ? 1 : 0;
+            float4* P = p.partial + ((long long)w * 2 + slot) * (kTPW * NT * 32) + lane;
+#pragma unroll
+            for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    __stcg(P + (it * NT + nt) * 32,
+                           make_float4(acc[it][nt][0], acc[it][nt][1], acc[it][nt][2], acc[it][nt][3]));
+            __threadfence();
+            int prev = 0;
+            if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
+            prev = __shfl_sync(0xffffffffu, prev, 0);
+            if (prev != last - first) continue;
+            __threadfence();
+#pragma unroll
+            for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[it][nt][c] = 0.f;
+            for (int j = first; j <= last; ++j) {
+                const int sj = (j == first) ? 1 : 0;
+                const float4* Q = p.partial + ((long long)j * 2 + sj) * (kTPW * NT * 32) + lane;
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        const float4 v = __ldcg(Q + (it * NT + nt) * 32);
+                        acc[it][nt][0] += v.x;
+                        acc[it][nt][1] += v.y;
+                        acc[it][nt][2] += v.z;
+                        acc[it][nt][3] += v.w;
+                    }
+            }
+            if (lane == 0) p.counters[unit] = 0;
+        }
+        gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+    }
+}
+
+}  // namespace cascade

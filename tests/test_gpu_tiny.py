@@ -1,0 +1,222 @@
+"""GPU parity of the full verification step on the tiny config (BASELINE
+config 1: 8 experts top-2, 4 layers), through the C ABI, against the CPU
+oracle on identical counter-hash weights.
+
+Bars:
+  * weights: bit-exact (same hash, device layout undone by read-back)
+  * router top-k, expert union, greedy argmax and accepted counts: exact,
+    except where the oracle's own decision margin is below MARGIN (flagged)
+  * logits / layer outputs: |gpu - oracle| <= ATOL + RTOL * max|oracle|
+"""
+
+import numpy as np
+import pytest
+
+import paper_2506_20675_b200 as cb
+from oracle.oracle import OracleModel, OracleSession, greedy_accept, union
+
+pytestmark = pytest.mark.gpu
+
+SEED = cb.TINY_SEED
+MARGIN = 2e-3      # decision margins below this are flagged, not failed
+LOGIT_RTOL = 1e-2  # of max |logit|
+LOGIT_ATOL = 2e-3
+
+
+def bf2f(a):
+    return (np.asarray(a, np.uint32) << 16).view(np.float32)
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    shape = cb.preset("tiny")
+    m = cb.Model(shape, SEED)
+    om = OracleModel(shape, SEED)
+    yield shape, m, om
+    m.close()
+
+
+def prompt(n=48, seed=3):
+    rng = np.random.default_rng(seed)
+    base = rng.integers(0, 1024, 12)
+    return np.concatenate([base, base[:5], rng.integers(0, 1024, n - 17)]).astype(np.int32)
+
+
+def test_device_weights_bit_exact(tiny):
+    shape, m, om = tiny
+    d, f, hq, kvd = shape.d_model, shape.d_ff, shape.n_heads * shape.head_dim, shape.n_kv_heads * shape.head_dim
+    cases = [
+        (cb.T_EMBED, 0, 0, 0, 50, d),
+        (cb.T_ATTN_NORM, 1, 0, 0, 1, d),
+        (cb.T_FFN_NORM, 3, 0, 0, 1, d),
+        (cb.T_WQ, 0, 0, 0, hq, d),
+        (cb.T_WK, 2, 0, 0, kvd, d),
+        (cb.T_WV, 3, 0, 0, kvd, d),
+        (cb.T_WO, 1, 0, 0, d, hq),
+        (cb.T_ROUTER, 2, 0, 0, shape.experts_per_layer, d),
+        (cb.T_W_GATE, 1, 5, 0, f, d),
+        (cb.T_W_UP, 1, 5, 0, f, d),
+        (cb.T_W_DOWN, 3, 7, 0, d, f),
+        (cb.T_LM_HEAD, 0, 0, 100, 64, d),
+        (cb.T_FINAL_NORM, 0, 0, 0, 1, d),
+    ]
+    for kind, layer, expert, row0, n, cols in cases:
+        g = m.read_weight(kind, layer, expert, row0, n, cols)
+        o = om.tensor(kind, layer, expert, row0, n, cols)
+        assert np.array_equal(g, o), (kind, layer, expert)
+
+
+def test_teacher_forced_stages(tiny):
+    """One verify step with debug taps; every stage checked against the oracle
+    fed the device's own stage inputs (so errors do not compound)."""
+    shape, m, om = tiny
+    s = cb.Session(m, max_ctx=256, k_max=8)
+    p = prompt()
+    s.prefill(p)
+    ctx = len(p) - 1
+    s.enable_taps(True)
+    drafts = np.array([11, 22, 33, 44, 55, 66, 77, 88], np.int32)
+    out = s.verify(drafts)
+    T = len(drafts) + 1
+    x_in, x_mid = s.tap("x_in"), s.tap("x_mid")
+    xn_attn, xn_moe = s.tap("xn_attn"), s.tap("xn_moe")
+    rl, tid, tw, moe = s.tap("router_logits"), s.tap("topk_id"), s.tap("topk_w"), s.tap("moe_out")
+    flagged = 0
+    for l in range(shape.num_layers):
+        kc = s.read_kv(l, 0, ctx + T)
+        vc = s.read_kv(l, 1, ctx + T)
+        # attention input norm: bf16 outputs may differ by one ulp at rounding ties
+        ox = om.rmsnorm(cb.T_ATTN_NORM, l, x_in[l, :T])
+        diff = np.abs(ox.astype(np.int32) - xn_attn[l, :T].astype(np.int32))
+        assert diff.max() <= 1 and (diff > 0).mean() < 0.01
+        # attention block (RoPE, KV append, causal GQA, O-proj)
+        oa, kn, vn = om.attention(l, x_in[l, :T], ctx, kc[:, :ctx], vc[:, :ctx])
+        ga = x_mid[l, :T].astype(np.float64) - x_in[l, :T]
+        assert np.abs(ga - oa).max() <= 1e-3 + 1e-2 * np.abs(oa).max()
+        # appended KV rows (bf16, may differ by one ulp)
+        dk = np.abs(bf2f(kc[:, ctx:ctx + T]) - bf2f(kn))
+        assert dk.max() <= 1e-2 * max(1.0, np.abs(bf2f(kn)).max())
+        # router on the device's MoE input
+        ox2 = om.rmsnorm(cb.T_FFN_NORM, l, x_mid[l, :T])
+        assert np.abs(ox2.astype(np.int32) - xn_moe[l, :T].astype(np.int32)).max() <= 1
+        logits, topk, topw, gsh, margin = om.router(l, xn_moe[l, :T])
+        E = shape.experts_per_layer
+        assert np.abs(rl[l, :T, :E] - logits[:, :E]).max() <= 1e-4 * max(1, np.abs(logits).max())
+        for t in range(T):
+            if margin[t] < MARGIN:
+                flagged += 1
+                continue
+            assert list(tid[l, t]) == list(topk[t]), (l, t)
+            assert np.allclose(tw[l, t], topw[t], rtol=1e-5, atol=1e-6)
+        # expert union of the step equals the oracle's union
+        assert sorted(set(tid[l, :T].ravel())) == list(union(tid[l, :T]))
+        # MoE block on the device routing
+        om_out = om.moe(l, xn_moe[l, :T], tid[l, :T], tw[l, :T].astype(np.float64), gsh)
+        assert np.abs(moe[l, :T] - om_out).max() <= 1e-3 + 1e-2 * np.abs(om_out).max()
+    # LM head on the device's final norm input (x after last layer = x_mid + moe)
+    x_last = x_mid[-1, :T].astype(np.float64) + moe[-1, :T]
+    xf = om.rmsnorm(cb.T_FINAL_NORM, 0, x_last.astype(np.float32))
+    lg, am, mg = om.lm_head(xf)
+    glog = s.tap("final_logits")[:T]
+    assert np.abs(glog - lg).max() <= LOGIT_ATOL + LOGIT_RTOL * np.abs(lg).max()
+    for t in range(T):
+        if mg[t] >= MARGIN:
+            assert out.argmax[t] == am[t]
+    acc, _ = greedy_accept(np.array(out.argmax[:T]), drafts)
+    assert out.accepted == acc
+    assert flagged <= T  # near-ties are rare with router_scale 4
+    s.close()
+
+
+def greedy_sequence(om, p, n):
+    os_ = OracleSession(om, 512)
+    os_.prefill(p)
+    seq = []
+    for _ in range(n):
+        acc, am, lg, mg, us = os_.verify([])
+        seq.append(int(am[0]))
+    return seq
+
+
+@pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
+def test_end_to_end_greedy_decode(tiny, K):
+    """Lock-step decode, device vs independent oracle (no teacher forcing):
+    drafts are the true greedy continuation with random corruptions, so
+    every accepted count 0..K occurs.  Argmax rows, accepted counts, KV
+    length and per-layer union sizes must agree exactly."""
+    shape, m, om = tiny
+    p = prompt(40, seed=10 + K)
+    truth = greedy_sequence(om, p, 80)
+    s = cb.Session(m, max_ctx=512, k_max=8)
+    s.prefill(p)
+    os_ = OracleSession(om, 512)
+    os_.prefill(p)
+    rng = np.random.default_rng(K)
+    pos = 0  # index into truth of the next token to be emitted
+    steps = 0
+    while pos + K < len(truth) and steps < 30:
+        drafts = np.array(truth[pos: pos + K], np.int32)
+        for i in range(K):
+            if rng.random() < 0.3:
+                drafts[i] = rng.integers(0, shape.vocab)
+        g = s.verify(drafts)
+        acc, am, lg, mg, us = os_.verify(drafts)
+        T = K + 1
+        if np.any(mg[:T] < MARGIN):
+            break  # flagged near-tie: the two decodes may legitimately diverge
+        assert list(g.argmax[:T]) == list(am), steps
+        assert g.accepted == acc
+        assert g.emitted == acc + 1
+        assert g.cache_len == os_.cache_len
+        assert list(s.union_sizes()) == list(us)
+        assert list(g.tokens[: acc + 1]) == list(truth[pos: pos + acc + 1])
+        pos += acc + 1
+        steps += 1
+    assert steps >= 10
+    s.close()
+
+
+def test_graph_replay_matches_eager(tiny):
+    shape, m, om = tiny
+    p = prompt(33, seed=5)
+    res = []
+    for taps in (False, True):
+        s = cb.Session(m, max_ctx=256, k_max=8)
+        if taps:
+            s.enable_taps(True)
+        s.prefill(p)
+        outs = []
+        for K in (3, 0, 8, 2):
+            o = s.verify(np.arange(1, K + 1, dtype=np.int32) * 7)
+            outs.append((o.accepted, list(o.argmax[: K + 1]), o.cache_len, list(s.union_sizes())))
+        res.append(outs)
+        s.close()
+    assert res[0] == res[1]
+
+
+def test_rejects_bad_requests(tiny):
+    shape, m, om = tiny
+    s = cb.Session(m, max_ctx=64, k_max=4)
+    with pytest.raises(ValueError):
+        s.verify(np.arange(5, dtype=np.int32))  # K > k_max
+    with pytest.raises(ValueError):
+        s.prefill(np.array([5000], np.int32))  # token out of range
+    with pytest.raises(ValueError):
+        s.set_baseline(0.0)
+    s.close()
+
+
+def test_utility_and_cost_breakdown(tiny):
+    """CostBreakdown parts sum to total (expert_model_test.cpp:120-133) and
+    the on-device utility equals emitted * t_base / total."""
+    shape, m, om = tiny
+    s = cb.Session(m, max_ctx=256, k_max=8)
+    s.prefill(prompt(20, seed=9))
+    s.set_baseline(1.0e6)
+    o = s.verify(np.array([1, 2, 3], np.int32), draft_ns=1234.0)
+    assert o.total == pytest.approx(o.attention_time + o.expert_time + o.draft_time + o.sampling_time, rel=1e-12)
+    assert o.draft_time == 1234.0
+    assert o.attention_time > 0 and o.expert_time > 0 and o.sampling_time > 0
+    assert o.utility == pytest.approx(o.emitted * 1.0e6 / o.total, rel=1e-12)
+    assert shape.top_k <= o.active_experts_per_layer <= shape.experts_per_layer
+    s.close()
