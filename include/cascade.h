@@ -220,9 +220,11 @@ CASCADE_API int cascade_read_kv(cascade_session* s, int layer, int which, int le
  * n-gram (prompt-lookup) drafter + utility-driven test-and-set controller
  * (controller.hpp:81-321) or a static K.  `policy` = -1: adaptive, k >= 0:
  * static k.  Writes generated tokens to out_tokens (capacity max_new) and,
- * when `telemetry` is non-NULL, one row per iteration:
- *   {iter, k_used, tokens_emitted, draft_ns, verify_ns, sampling_ns, total_ns, tag, trial}
- * as 9 doubles.  Returns the number of iterations via *n_iters. */
+ * when `telemetry` is non-NULL, one row per iteration (IterationRecord,
+ * utility.hpp:32-42, plus the drafts actually offered):
+ *   {iter, k_used, tokens_emitted, draft_ns, verify_ns, sampling_ns, total_ns, tag, trial, k_offered}
+ * as 10 doubles.  The session is reset first; its max_ctx must hold the
+ * prompt plus max_new + 32 tokens.  Returns the number of iterations via *n_iters. */
 typedef struct cascade_decode_cfg {
     int32_t policy;            /* -1 adaptive, else static K */
     int32_t max_new;           /* tokens to generate */

@@ -384,14 +384,16 @@ int orc_moe(orc_model* m, int layer, const uint16_t* xn, int T, const int32_t* t
     if (!m || !xn || !topk || !topw || !out || T < 1) return -1;
     const int d = m->d, k = m->k;
     double* x = bf_to_d(xn, (long)T * d);
-    double* xs = (double*)malloc((size_t)T * d * sizeof(double));
-    double* ys = (double*)malloc((size_t)T * d * sizeof(double));
+    double* xs = (double*)malloc((size_t)T * k * d * sizeof(double));
+    double* ys = (double*)malloc((size_t)T * k * d * sizeof(double));
     double* routed = (double*)calloc((size_t)T * k * d, sizeof(double)); /* [t][r][d] */
     int32_t uniq[128];
     const int U = orc_union(topk, T, k, uniq);
     for (int ui = 0; ui < U; ++ui) {
         const int e = uniq[ui];
-        int toks[64], ranks[64], n = 0;
+        int* toks = (int*)malloc((size_t)T * k * sizeof(int));
+        int* ranks = (int*)malloc((size_t)T * k * sizeof(int));
+        int n = 0;
         for (int t = 0; t < T; ++t)
             for (int r = 0; r < k; ++r)
                 if (topk[t * k + r] == e) {
@@ -403,6 +405,8 @@ int orc_moe(orc_model* m, int layer, const uint16_t* xn, int T, const int32_t* t
         expert_ffn(m, layer, e, xs, n, ys);
         for (int i = 0; i < n; ++i)
             memcpy(routed + ((long)toks[i] * k + ranks[i]) * d, ys + (long)i * d, d * sizeof(double));
+        free(toks);
+        free(ranks);
     }
     double* shared = NULL;
     if (m->S > 0) {
@@ -466,48 +470,62 @@ static int attention_d(orc_model* m, int layer, const double* xd, int T, int ctx
             }
         }
     }
-    const int nk = ctx + T;
-    double* sc = (double*)malloc((size_t)nk * sizeof(double));
-    double* o = (double*)malloc((size_t)T * H * hd * sizeof(double));
+    /* Device precision contract (attention.cuh): q is rotated, scaled by
+     * 1/sqrt(hd) and rounded to bf16; keys are split into 64-key chunks of
+     * the cache plus one chunk of the T new tokens; inside a chunk the
+     * probabilities exp(s - m_chunk) enter P*V rounded to bf16 while the
+     * chunk sum uses them unrounded; chunks merge with the usual rescaling. */
     const double scale = 1.0 / sqrt((double)hd);
+    double* o = (double*)malloc((size_t)T * H * hd * sizeof(double));
+    double* qs = (double*)malloc((size_t)hd * sizeof(double));
+    double* sc = (double*)malloc(64 * sizeof(double));
+    double* oc = (double*)malloc((size_t)hd * sizeof(double));
+    const int nch = (ctx + 63) / 64;
     for (int t = 0; t < T; ++t)
         for (int h = 0; h < H; ++h) {
             const int kvh = h / G;
             const double* qv = q + ((long)t * H + h) * hd;
-            const int n = ctx + t + 1;
-            double mx = -INFINITY;
-            for (int j = 0; j < n; ++j) {
-                double s = 0;
-                if (j < ctx) {
-                    const uint16_t* kr = kc + ((long)kvh * kc_stride + j) * hd;
-                    for (int i = 0; i < hd; ++i) s += qv[i] * bf(kr[i]);
-                } else {
-                    const double* kr = kk + ((long)(j - ctx) * KV + kvh) * hd;
-                    for (int i = 0; i < hd; ++i) s += qv[i] * kr[i];
-                }
-                s *= scale;
-                sc[j] = s;
-                mx = s > mx ? s : mx;
-            }
-            double z = 0;
-            for (int j = 0; j < n; ++j) {
-                sc[j] = exp(sc[j] - mx);
-                z += sc[j];
-            }
+            for (int i = 0; i < hd; ++i) qs[i] = bf(d2bf(qv[i] * scale));
+            double M = -INFINITY, L = 0;
             double* ov = o + ((long)t * H + h) * hd;
             for (int i = 0; i < hd; ++i) ov[i] = 0;
-            for (int j = 0; j < n; ++j) {
-                const double p = sc[j] / z;
-                if (j < ctx) {
-                    const uint16_t* vr = vc + ((long)kvh * kc_stride + j) * hd;
-                    for (int i = 0; i < hd; ++i) ov[i] += p * bf(vr[i]);
-                } else {
-                    const double* vr = vv + ((long)(j - ctx) * KV + kvh) * hd;
-                    for (int i = 0; i < hd; ++i) ov[i] += p * vr[i];
+            for (int c = 0; c <= nch; ++c) {
+                const int is_new = c == nch;
+                const int j0 = is_new ? 0 : c * 64;
+                const int nkeys = is_new ? t + 1 : ((ctx - j0) < 64 ? (ctx - j0) : 64);
+                double mc = -INFINITY;
+                for (int j = 0; j < nkeys; ++j) {
+                    const double* kn_ = is_new ? kk + ((long)j * KV + kvh) * hd : NULL;
+                    const uint16_t* kr = is_new ? NULL : kc + ((long)kvh * kc_stride + j0 + j) * hd;
+                    double s2 = 0;
+                    for (int i = 0; i < hd; ++i) s2 += qs[i] * (is_new ? kn_[i] : bf(kr[i]));
+                    sc[j] = s2;
+                    mc = s2 > mc ? s2 : mc;
                 }
+                double lc = 0;
+                for (int i = 0; i < hd; ++i) oc[i] = 0;
+                for (int j = 0; j < nkeys; ++j) {
+                    const double e = exp(sc[j] - mc);
+                    lc += e;
+                    const double pb = bf(d2bf(e));
+                    const double* vn_ = is_new ? vv + ((long)j * KV + kvh) * hd : NULL;
+                    const uint16_t* vr = is_new ? NULL : vc + ((long)kvh * kc_stride + j0 + j) * hd;
+                    for (int i = 0; i < hd; ++i) oc[i] += pb * (is_new ? vn_[i] : bf(vr[i]));
+                }
+                if (mc > M) {
+                    const double r = exp(M - mc);
+                    L *= r;
+                    for (int i = 0; i < hd; ++i) ov[i] *= r;
+                    M = mc;
+                }
+                const double r = exp(mc - M);
+                L += lc * r;
+                for (int i = 0; i < hd; ++i) ov[i] += oc[i] * r;
             }
-            for (int i = 0; i < hd; ++i) ov[i] = bf(d2bf(ov[i])); /* O-proj input is bf16 */
+            for (int i = 0; i < hd; ++i) ov[i] = bf(d2bf(ov[i] / L)); /* O-proj input is bf16 */
         }
+    free(oc);
+    free(qs);
     linear(m, W(m, CASCADE_T_WO, layer, 0), d, H * hd, o, T, out);
     free(o);
     free(sc);

@@ -1,12 +1,16 @@
-// ref_shim.cpp — extern "C" shim over the UNMODIFIED reference headers.
+// specsim_shim.cpp — extern "C" shim over a `specsim` header set.
 //
-// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile (`make ref`) from
-// the headers where they lie under /root/reference/proj/include (and the
-// reference's test harness, /root/reference/proj/tests/landscape_harness.hpp)
-// into oracle/_ref/libspecsim_ref.so.  Used (1) to generate the golden
-// vectors committed under tests/golden/ (tests/golden/make_golden.py) and
-// (2) as the reference CPU pricing of the step in bench.py.  Nothing here
-// is copied from the reference; the shim only calls it.
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles it twice:
+//  * `make ref`  -> oracle/_ref/libspecsim_ref.so against the UNMODIFIED
+//    reference headers where they lie (/root/reference/proj/include, plus
+//    the reference harness /root/reference/proj/tests/landscape_harness.hpp);
+//  * `make ours` -> oracle/libspecsim_ours.so against this repository's
+//    include/specsim (plus tests/cpp/landscape_harness.hpp).
+// tests/test_specsim_parity.py calls both with identical inputs and
+// requires identical outputs; tests/golden/make_golden.py records the
+// reference's outputs as committed golden vectors; bench.py times the
+// reference build as the reference CPU path.  Nothing here is copied from
+// the reference; the shim only calls the API.
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -171,6 +175,46 @@ int ref_run_request(double p, double affinity, int out_len, int policy, const ch
         out[5] = m.etr;
         out[6] = m.cost;
         out[7] = m.utility;
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// Replays recorded iterations (tokens, total time) through a fresh
+// controller; writes the k the controller chose before each record and its
+// tag.  Used to check the GPU decode loop's K trace (cascade_decode with an
+// injected cost) against this controller.
+int ref_controller_replay(const int32_t* cfg_i, double band, int n, const int32_t* tokens, const double* total,
+                          int32_t* k_out, int32_t* tag_out) {
+    try {
+        ControllerConfig cfg;
+        cfg.t_trial = cfg_i[0];
+        cfg.max_trials = cfg_i[1];
+        cfg.s_set = cfg_i[2];
+        cfg.s_cap = cfg_i[3];
+        cfg.k_max = cfg_i[4];
+        cfg.k_start = cfg_i[5];
+        cfg.baseline_refresh_interval = cfg_i[6];
+        cfg.baseline_probe_len = cfg_i[7];
+        cfg.backoff_enabled = cfg_i[8] != 0;
+        cfg.convergence_band = band;
+        SpeculationController ctl(cfg);
+        UtilityAnalyzer an(16);
+        for (int i = 0; i < n; ++i) {
+            IterationRecord r;
+            r.iter_index = i;
+            r.k_used = ctl.current_k();
+            r.tag = ctl.current_tag();
+            r.trial_no = ctl.current_trial();
+            r.tokens_emitted = tokens[i];
+            if (r.tokens_emitted > r.k_used + 1) r.tokens_emitted = r.k_used + 1;
+            r.total_time = total[i];
+            r.verify_time = total[i];
+            k_out[i] = r.k_used;
+            tag_out[i] = (int32_t)r.tag;
+            ctl.next_k(r, an);
+        }
         return 0;
     } catch (...) {
         return -1;

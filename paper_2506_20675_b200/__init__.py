@@ -155,6 +155,7 @@ class ModelShape:
         expert = 3 * d * f * 2
         out = {"experts": 0, "dense": 0, "kv": 0, "head": 0}
         for u in union_sizes:
+            u = int(u)
             out["experts"] += (u + self.shared_experts) * expert
             out["dense"] += (d * (hq + 2 * kvd) + hq * d) * 2 + (self.experts_per_layer + self.shared_gate) * d * 2 + 2 * d * 2
             out["kv"] += ctx * 2 * kvd * 2 + T * 2 * kvd * 2
@@ -435,7 +436,7 @@ class Session:
         out = np.zeros(cfg.max_new + MAX_TOKENS, np.int32)
         n_out = ctypes.c_int32()
         n_it = ctypes.c_int32()
-        tel = np.zeros((max(telemetry_cap, 1), 9), np.float64)
+        tel = np.zeros((max(telemetry_cap, 1), 10), np.float64)
         _check(lib().cascade_decode(self.h, _i32p(p), len(p), ctypes.byref(cfg), _i32p(out), ctypes.byref(n_out),
                                     tel.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if telemetry_cap else None,
                                     telemetry_cap, ctypes.byref(n_it)))

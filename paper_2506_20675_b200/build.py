@@ -54,7 +54,7 @@ def build_cascade(force: bool = False, verbose: bool = False) -> str:
 
 def build_oracle(force: bool = False) -> str:
     odir = os.path.join(ROOT, "oracle")
-    args = ["make", "-s", "-C", odir, "liboracle.so"]
+    args = ["make", "-s", "-C", odir, "liboracle.so", "libspecsim_ours.so"]
     if force:
         args.insert(1, "-B")
     subprocess.check_call(args)

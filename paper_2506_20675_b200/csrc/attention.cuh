@@ -30,20 +30,17 @@ struct AttnParams {
     uint16_t* kc;            // [KV][max_ctx][hd] bf16 (this layer)
     uint16_t* vc;
     const int* ctx_ptr;      // committed cache length
+    const float2* rope;      // [T][hd/2] (cos, sin) at position ctx + t (embed kernel)
     float* part;             // [KV][R][max_chunks][hd + 2]
     int T, H, KV, max_ctx, max_chunks;
-    double rope_theta;
     float scale;             // 1/sqrt(hd)
 };
 
-__device__ __forceinline__ void rope_pair(float& a, float& b, int pos, int i, int hd, double theta) {
-    const double inv = pow(theta, -2.0 * (double)i / (double)hd);
-    double sn, cs;
-    sincos((double)pos * inv, &sn, &cs);
-    const float c = (float)cs, s = (float)sn;
+// rotate_half RoPE on the pair (i, i + hd/2)
+__device__ __forceinline__ void rope_pair(float& a, float& b, float2 cs) {
     const float x0 = a, x1 = b;
-    a = x0 * c - x1 * s;
-    b = x1 * c + x0 * s;
+    a = x0 * cs.x - x1 * cs.y;
+    b = x1 * cs.x + x0 * cs.y;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -68,6 +65,8 @@ constexpr int attn_smem_bytes() {
 //   q [kAttnMaxRows][HD+8] | k [kChunk][HD+8] | v [kChunk][HD+8]
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
+    griddep_wait();
+    griddep_launch();
     constexpr int LD = HD + 8;
     constexpr int HALF = HD / 2;
     constexpr int NKS = HD / 16;      // k-steps of QK^T
@@ -104,7 +103,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 const int h = kvh * G + gi;
                 a = p.qkv[(long long)t * QD + h * HD + i];
                 b = p.qkv[(long long)t * QD + h * HD + i + HALF];
-                rope_pair(a, b, ctx + t, i, HD, p.rope_theta);
+                rope_pair(a, b, p.rope[t * HALF + i]);
                 a *= p.scale;
                 b *= p.scale;
             }
@@ -119,7 +118,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                     const float* kr = p.qkv + (long long)j * QD + p.H * HD + kvh * HD;
                     const float* vr = p.qkv + (long long)j * QD + (p.H + p.KV) * HD + kvh * HD;
                     float a = kr[i], b = kr[i + HALF];
-                    rope_pair(a, b, ctx + j, i, HD, p.rope_theta);
+                    rope_pair(a, b, p.rope[j * HALF + i]);
                     ka = bf16_bits(a);
                     kb = bf16_bits(b);
                     va = bf16_bits(vr[i]);
@@ -261,6 +260,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
 }
 
 // Merge chunk partials in fixed order; write bf16 O-proj input (B-frag).
+// One CTA per (token, head); the per-chunk (max, sum) pairs are staged in
+// shared memory so every o-load of the merge is independent.
 struct AttnCombineParams {
     const float* part;
     const int* ctx_ptr;
@@ -269,28 +270,42 @@ struct AttnCombineParams {
     int T, H, KV, hd, max_chunks;
 };
 
+constexpr int kMaxChunksSmem = 1024;
+
 __global__ void attn_combine_kernel(AttnCombineParams p) {
+    griddep_wait();
+    griddep_launch();
+    __shared__ float scale_c[kMaxChunksSmem];
+    __shared__ float red[32];
     const int t = blockIdx.x, h = blockIdx.y;
     const int G = p.H / p.KV;
     const int kvh = h / G, gi = h - kvh * G;
     const int R = G * p.T;
     const int r = gi * p.T + t;
     const int ctx = *p.ctx_ptr;
-    const int nch = (ctx + kChunk - 1) / kChunk;
-    const float* base = p.part + ((long long)kvh * R + r) * p.max_chunks * (p.hd + 2);
+    const int nch = (ctx + kChunk - 1) / kChunk + 1;
+    const int stride = p.hd + 2;
+    const float* base = p.part + ((long long)kvh * R + r) * p.max_chunks * stride;
+    float m = -INFINITY;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) m = fmaxf(m, base[(long long)c * stride]);
+    // block max
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
     float M = -INFINITY;
-    for (int c = 0; c <= nch; ++c) M = fmaxf(M, base[(long long)c * (p.hd + 2)]);
-    float L = 0.f;
-    for (int c = 0; c <= nch; ++c) {
-        const float* b = base + (long long)c * (p.hd + 2);
-        L += b[1] * __expf(b[0] - M);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, red[w]);
+    __syncthreads();
+    float l = 0.f;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        const float sc = __expf(base[(long long)c * stride] - M);
+        scale_c[c] = sc;
+        l += base[(long long)c * stride + 1] * sc;
     }
+    const float L = block_sum(l, red);  // syncs: scale_c visible
     for (int i = threadIdx.x; i < p.hd; i += blockDim.x) {
         float o = 0.f;
-        for (int c = 0; c <= nch; ++c) {
-            const float* b = base + (long long)c * (p.hd + 2);
-            o += b[2 + i] * __expf(b[0] - M);
-        }
+#pragma unroll 4
+        for (int c = 0; c < nch; ++c) o += base[(long long)c * stride + 2 + i] * scale_c[c];
         const float v = o / L;
         const int k = h * p.hd + i;
         p.out_bfrag[bfrag_index(t, k)] = bf16_bits(v);

@@ -59,6 +59,9 @@ extern "C" size_t cascade_last_error(char* buf, size_t n) {
     return g_err.size();
 }
 
+// internal (hidden): lets decode.cpp report through the same error slot
+extern "C" int cascade_internal_set_error(int code, const char* msg) { return set_err(code, msg ? msg : ""); }
+
 extern "C" const char* cascade_build_info(void) { return "sm_100a " CASCADE_GIT; }
 
 // ---------------------------------------------------------------- NCCL (dlopen)
@@ -386,6 +389,7 @@ struct AcceptParams {
 };
 
 __global__ void accept_kernel(AcceptParams p) {
+    griddep_wait();
     if (threadIdx.x != 0) return;
     const uint64_t t_end = globaltimer();
     cascade_verify_out r;
@@ -438,6 +442,18 @@ __global__ void accept_kernel(AcceptParams p) {
     *p.res = r;
 }
 
+template <int NT>
+static cudaError_t gemv_smem_attr() {
+    const int sm = gemv_smem_bytes<NT>();
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_kernel<NT, EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_kernel<NT, EPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_kernel<NT, EPI_GATEUP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_kernel<NT, EPI_DOWN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_kernel<NT, EPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    return e;
+}
+
 // ---------------------------------------------------------------- session
 struct Taps {
     uint16_t* xn_moe = nullptr;   // [L][16][d]
@@ -483,6 +499,7 @@ struct cascade_session {
     unsigned long long* keys = nullptr;
     unsigned long long* stamps = nullptr;
     int* tokens_used = nullptr;
+    float2* rope = nullptr;
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -529,6 +546,10 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     s->max_ctx = max_ctx + kMaxT;  // room for the in-flight rows
     s->k_max = k_max;
     s->max_chunks = (s->max_ctx + kChunk - 1) / kChunk + 1;
+    if (s->max_chunks > kMaxChunksSmem) {
+        delete s;
+        return set_err(CASCADE_EINVAL, "max_ctx too large (limit 65000 positions)");
+    }
     if (stream) {
         s->stream = (cudaStream_t)stream;
     } else {
@@ -571,6 +592,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->partial, (size_t)workers * 2 * kTPW * 2 * 32 * 16, false)) ||
         (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
+        (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
         (rc = salloc(s, &s->kc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)) ||
         (rc = salloc(s, &s->vc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)))
         return fail(rc);
@@ -587,6 +609,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     else if (D.hd == 64) e = cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+    if (e == cudaSuccess) e = gemv_smem_attr<1>();
+    if (e == cudaSuccess) e = gemv_smem_attr<2>();
     if (e == cudaSuccess && D.d * 4 > 48 * 1024)
         e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D.d * 4);
     if (e != cudaSuccess) {
@@ -605,20 +629,41 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
 extern "C" void* cascade_session_stream(cascade_session* s) { return s ? (void*)s->stream : nullptr; }
 
 // ------------------------------------------------------------ step enqueue
+// Every kernel of the step is launched with programmatic stream
+// serialisation (PDL): it may be scheduled while its predecessor drains and
+// blocks in griddepcontrol.wait until the predecessor's memory is visible.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int NT>
-static void launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaStream_t st) {
+static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaStream_t st, bool pdl) {
+    const size_t sm = gemv_smem_bytes<NT>();
     switch (epi) {
-    case EPI_STORE: stream_gemv_kernel<NT, EPI_STORE><<<grid, kGemvThreads, 0, st>>>(p); break;
-    case EPI_ADD: stream_gemv_kernel<NT, EPI_ADD><<<grid, kGemvThreads, 0, st>>>(p); break;
-    case EPI_GATEUP: stream_gemv_kernel<NT, EPI_GATEUP><<<grid, kGemvThreads, 0, st>>>(p); break;
-    case EPI_DOWN: stream_gemv_kernel<NT, EPI_DOWN><<<grid, kGemvThreads, 0, st>>>(p); break;
-    case EPI_ARGMAX: stream_gemv_kernel<NT, EPI_ARGMAX><<<grid, kGemvThreads, 0, st>>>(p); break;
+    case EPI_STORE: return launch_k(stream_gemv_kernel<NT, EPI_STORE>, grid, kGemvThreads, sm, st, pdl, p);
+    case EPI_ADD: return launch_k(stream_gemv_kernel<NT, EPI_ADD>, grid, kGemvThreads, sm, st, pdl, p);
+    case EPI_GATEUP: return launch_k(stream_gemv_kernel<NT, EPI_GATEUP>, grid, kGemvThreads, sm, st, pdl, p);
+    case EPI_DOWN: return launch_k(stream_gemv_kernel<NT, EPI_DOWN>, grid, kGemvThreads, sm, st, pdl, p);
+    default: return launch_k(stream_gemv_kernel<NT, EPI_ARGMAX>, grid, kGemvThreads, sm, st, pdl, p);
     }
 }
-static void launch_gemv(int epi, const GemvParams& p, int grid, cudaStream_t st) {
-    if (p.T <= 8) launch_gemv_nt<1>(epi, p, grid, st);
-    else launch_gemv_nt<2>(epi, p, grid, st);
+static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStream_t st, bool pdl = true) {
+    return p.T <= 8 ? launch_gemv_nt<1>(epi, p, grid, st, pdl) : launch_gemv_nt<2>(epi, p, grid, st, pdl);
 }
+
+
 
 static GemvParams gemv_base(cascade_session* s, int T) {
     GemvParams p{};
@@ -675,11 +720,14 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ep.stamp = s->stamps;
     ep.tap_x = taps ? s->taps.x_in : nullptr;
     ep.tap_xn = taps ? s->taps.xn_attn : nullptr;
+    ep.rope = s->rope;
     ep.T = T;
     ep.d = D.d;
+    ep.hd = D.hd;
+    ep.rope_theta = (double)m->g.rope_theta;
     ep.eps = m->g.norm_eps;
     PB(0);
-    embed_norm_kernel<<<T, kRouteThreads, 0, st>>>(ep);
+    CK(launch_k(embed_norm_kernel, dim3(T), dim3(kRouteThreads), 0, st, false, ep));
     PE();
     ++nk;
 
@@ -697,7 +745,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         q.ld = D.qkvd;
         q.stamp = s->stamps + 1 + 2 * l;
         PB(1);
-        launch_gemv(EPI_STORE, q, s->gemv_grid, st);
+        CK(launch_gemv(EPI_STORE, q, s->gemv_grid, st));
         PE();
         ++nk;
         // attention
@@ -706,19 +754,19 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ap.kc = s->kc + (size_t)l * D.KV * s->max_ctx * D.hd;
         ap.vc = s->vc + (size_t)l * D.KV * s->max_ctx * D.hd;
         ap.ctx_ptr = &s->d_state->cache_len;
+        ap.rope = s->rope;
         ap.part = s->attn_part;
         ap.T = T;
         ap.H = D.H;
         ap.KV = D.KV;
         ap.max_ctx = s->max_ctx;
         ap.max_chunks = s->max_chunks;
-        ap.rope_theta = (double)m->g.rope_theta;
         ap.scale = 1.0f / sqrtf((float)D.hd);
         const int agrid = m->num_sms;
         PB(2);
-        if (D.hd == 32) attn_partial_kernel<32><<<agrid, kAttnThreads, attn_smem_bytes<32>(), st>>>(ap);
-        else if (D.hd == 64) attn_partial_kernel<64><<<agrid, kAttnThreads, attn_smem_bytes<64>(), st>>>(ap);
-        else attn_partial_kernel<128><<<agrid, kAttnThreads, attn_smem_bytes<128>(), st>>>(ap);
+        if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, attn_smem_bytes<32>(), st, true, ap));
+        else if (D.hd == 64) CK(launch_k(attn_partial_kernel<64>, agrid, kAttnThreads, attn_smem_bytes<64>(), st, true, ap));
+        else CK(launch_k(attn_partial_kernel<128>, agrid, kAttnThreads, attn_smem_bytes<128>(), st, true, ap));
         PE();
         ++nk;
         AttnCombineParams cp{};
@@ -732,7 +780,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         cp.hd = D.hd;
         cp.max_chunks = s->max_chunks;
         PB(3);
-        attn_combine_kernel<<<dim3(T, D.H), D.hd, 0, st>>>(cp);
+        CK(launch_k(attn_combine_kernel, dim3(T, D.H), dim3(D.hd), 0, st, true, cp));
         PE();
         ++nk;
         (void)G;
@@ -745,7 +793,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         o.out = s->x;
         o.ld = D.d;
         PB(4);
-        launch_gemv(EPI_ADD, o, s->gemv_grid, st);
+        CK(launch_gemv(EPI_ADD, o, s->gemv_grid, st));
         PE();
         ++nk;
         if (taps) CK(cudaMemcpyAsync(s->taps.x_mid + td, s->x, (size_t)T * D.d * 4, cudaMemcpyDeviceToDevice, st));
@@ -781,7 +829,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.zero_nonlocal = m->ep_size > 1;
         rp.stamp = s->stamps + 2 + 2 * l;
         PB(5);
-        moe_route_kernel<<<T, kRouteThreads, D.d * 4, st>>>(rp);
+        const int rgroups = (D.E + (m->g.shared_gate ? 1 : 0) + kRouteWarps - 1) / kRouteWarps;
+        CK(launch_k(moe_route_kernel, dim3(T, rgroups), dim3(kRouteThreads), (size_t)D.d * 4, st, true, rp));
         PE();
         ++nk;
         if (taps) {
@@ -805,7 +854,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         gu.hout = s->hbuf;
         gu.h_block_stride = (long long)D.f * 16;
         PB(6);
-        launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st);
+        CK(launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st));
         PE();
         ++nk;
         GemvParams dn = gemv_base(s, T);
@@ -822,7 +871,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         dn.out = s->ycontrib;
         dn.ld = D.d;
         PB(7);
-        launch_gemv(EPI_DOWN, dn, s->gemv_grid, st);
+        CK(launch_gemv(EPI_DOWN, dn, s->gemv_grid, st));
         PE();
         ++nk;
         if (m->ep_size > 1) {
@@ -848,7 +897,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.S = D.S;
         c.eps = m->g.norm_eps;
         PB(8);
-        moe_combine_kernel<<<T, kRouteThreads, 0, st>>>(c);
+        CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRouteThreads), 0, st, m->ep_size == 1, c));
         PE();
         ++nk;
     }
@@ -863,7 +912,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     lm.ld = D.V;
     lm.stamp = s->stamps + 1 + 2 * D.L;
     PB(9);
-    launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st);
+    CK(launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st));
     PE();
     ++nk;
     AcceptParams ap{};
@@ -878,7 +927,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ap.L = D.L;
     ap.S = D.S;
     PB(10);
-    accept_kernel<<<1, 32, 0, st>>>(ap);
+    CK(launch_k(accept_kernel, dim3(1), dim3(32), 0, st, true, ap));
     PE();
     ++nk;
     CK(cudaGetLastError());

@@ -29,6 +29,13 @@ constexpr int kTPW = 4;                 // 16-row tiles per super-tile (per warp
 constexpr int kSTRows = 16 * kTPW;      // 64 rows per super-tile
 constexpr int kMaxT = 16;               // tokens in flight (two n8 tiles)
 
+// Programmatic dependent launch: every kernel of the step waits for its
+// predecessor's completion (and memory) before touching any data, so the
+// chain stays transitively ordered while launch latency and CTA
+// rasterisation overlap the predecessor's tail.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

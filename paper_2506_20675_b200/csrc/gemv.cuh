@@ -156,51 +156,104 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, int bl, int s
     }
 }
 
-// worker containing flat position q when [0,total) is split into n ranges
+// owner of flat position q when [0,total) is split into n ranges
 // [floor(total*w/n), floor(total*(w+1)/n))
-__device__ __forceinline__ int worker_of(long long q, long long total, int n) {
+__device__ __forceinline__ int owner_of(long long q, long long total, int n) {
     return (int)(((q + 1) * n + total - 1) / total) - 1;
 }
 
+template <int NT>
+__device__ __forceinline__ void zero_acc(float (&acc)[kTPW][NT][4]) {
+#pragma unroll
+    for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[it][nt][c] = 0.f;
+}
+
+template <int NT>
+__device__ __forceinline__ void add_acc(float (&acc)[kTPW][NT][4], const float4* src, bool cg) {
+#pragma unroll
+    for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const float4 v = cg ? __ldcg(src + (it * NT + nt) * 32) : src[(it * NT + nt) * 32];
+            acc[it][nt][0] += v.x;
+            acc[it][nt][1] += v.y;
+            acc[it][nt][2] += v.z;
+            acc[it][nt][3] += v.w;
+        }
+}
+
+template <int NT>
+__device__ __forceinline__ void store_acc(float4* dst, const float (&acc)[kTPW][NT][4], bool cg) {
+#pragma unroll
+    for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const float4 v = make_float4(acc[it][nt][0], acc[it][nt][1], acc[it][nt][2], acc[it][nt][3]);
+            if (cg) __stcg(dst + (it * NT + nt) * 32, v);
+            else dst[(it * NT + nt) * 32] = v;
+        }
+}
+
+template <int NT>
+constexpr int gemv_smem_bytes() {
+    return kGemvWarps * 2 * kTPW * NT * 32 * 16;
+}
+
+// Stream-K at two levels.  The flat work range is split into one
+// contiguous range per CTA, and each CTA range into one contiguous range
+// per warp.  A warp finishes every super-tile it covers completely
+// (epilogue straight from registers).  Super-tiles split between warps of
+// the same CTA are reduced through shared memory by their first
+// contributor in warp order; only the (at most two) super-tiles that cross
+// a CTA boundary go through global memory, where the last-arriving CTA
+// sums the CTA partials in CTA order.  Every summation order is a pure
+// function of (U, grid), so results are deterministic.
 template <int NT, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams p) {
+    griddep_wait();
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
+    extern __shared__ float4 red[];  // [warp][slot][kTPW*NT*32]
+    __shared__ long long seg_unit[kGemvWarps][2];
+    __shared__ int s_last;
+    constexpr int kSlot = kTPW * NT * 32;
     const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int U = p.count ? *p.count : p.n_blocks;
     const long long per_block = (long long)p.n_st * p.n_ks;
     const long long total = (long long)U * per_block;
     if (total <= 0) return;
-    long long nmax = total / p.min_seg;
-    if (nmax < 1) nmax = 1;
-    int N = gridDim.x * kGemvWarps;
-    if (N > nmax) N = (int)nmax;
-    const int w = blockIdx.x * kGemvWarps + (threadIdx.x >> 5);
-    if (w >= N) return;
-    const long long lo = total * w / N;
-    const long long hi = total * (w + 1) / N;
-
+    long long nc_max = total / ((long long)p.min_seg * kGemvWarps);
+    if (nc_max < 1) nc_max = 1;
+    const int NC = (long long)gridDim.x < nc_max ? (int)gridDim.x : (int)nc_max;
+    const int c = blockIdx.x;
+    if (c >= NC) return;
+    const long long clo = total * c / NC, chi = total * (c + 1) / NC;
+    const long long wlo = clo + (chi - clo) * warp / kGemvWarps;
+    const long long whi = clo + (chi - clo) * (warp + 1) / kGemvWarps;
+    if (lane == 0) {
+        seg_unit[warp][0] = -1;
+        seg_unit[warp][1] = -1;
+    }
+    __syncwarp();
     const uint64_t pol = policy_evict_first();
-    long long pos = lo;
-    while (pos < hi) {
+
+    float acc[kTPW][NT][4];
+    long long pos = wlo;
+    while (pos < whi) {
         const long long unit = pos / p.n_ks;
         const int ks0 = (int)(pos - unit * p.n_ks);
-        const long long rem = hi - pos;
+        const long long rem = whi - pos;
         const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
         const int bl = (int)(unit / p.n_st);
         const int st = (int)(unit - (long long)bl * p.n_st);
         const int blk = p.list ? p.list[bl] : bl;
-        const uint4* A = p.W + (long long)blk * p.w_block_stride +
-                         (long long)st * p.n_ks * (kTPW * 32) + lane;
+        const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
         const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
-
-        float acc[kTPW][NT][4];
-#pragma unroll
-        for (int it = 0; it < kTPW; ++it)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc[it][nt][c] = 0.f;
-
+        zero_acc<NT>(acc);
         int s = ks0;
         for (; s + kUnroll <= ks1; s += kUnroll) {
             uint4 a[kUnroll][kTPW];
@@ -233,51 +286,55 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[it], b[nt]);
         }
+        const bool first_seg = pos == wlo;
         pos += ks1 - ks0;
-
-        if (!(ks0 == 0 && ks1 == p.n_ks)) {
-            // split super-tile: publish the partial, last arriver reduces
-            const long long ustart = unit * p.n_ks;
-            const int first = worker_of(ustart, total, N);
-            const int last = worker_of(ustart + p.n_ks - 1, total, N);
-            const int slot = (w == first) ? 1 : 0;
-            float4* P = p.partial + ((long long)w * 2 + slot) * (kTPW * NT * 32) + lane;
-#pragma unroll
-            for (int it = 0; it < kTPW; ++it)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-                    __stcg(P + (it * NT + nt) * 32,
-                           make_float4(acc[it][nt][0], acc[it][nt][1], acc[it][nt][2], acc[it][nt][3]));
-            __threadfence();
-            int prev = 0;
-            if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
-            prev = __shfl_sync(0xffffffffu, prev, 0);
-            if (prev != last - first) continue;
-            __threadfence();
-#pragma unroll
-            for (int it = 0; it < kTPW; ++it)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[it][nt][c] = 0.f;
-            for (int j = first; j <= last; ++j) {
-                const int sj = (j == first) ? 1 : 0;
-                const float4* Q = p.partial + ((long long)j * 2 + sj) * (kTPW * NT * 32) + lane;
-#pragma unroll
-                for (int it = 0; it < kTPW; ++it)
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        const float4 v = __ldcg(Q + (it * NT + nt) * 32);
-                        acc[it][nt][0] += v.x;
-                        acc[it][nt][1] += v.y;
-                        acc[it][nt][2] += v.z;
-                        acc[it][nt][3] += v.w;
-                    }
-            }
-            if (lane == 0) p.counters[unit] = 0;
+        if (ks0 == 0 && ks1 == p.n_ks) {
+            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+        } else {
+            const int slot = first_seg ? 0 : 1;
+            store_acc<NT>(red + (warp * 2 + slot) * kSlot + lane, acc, false);
+            if (lane == 0) seg_unit[warp][slot] = unit;
         }
+    }
+    __syncthreads();
+
+    // ---- CTA-level reduction of split super-tiles (owner = first contributor)
+    for (int slot = 0; slot < 2; ++slot) {
+        const long long unit = seg_unit[warp][slot];
+        if (unit < 0) continue;
+        bool owner = true;
+        for (int w = 0; w < warp && owner; ++w) owner = seg_unit[w][0] != unit && seg_unit[w][1] != unit;
+        if (!owner) continue;
+        zero_acc<NT>(acc);
+        add_acc<NT>(acc, red + (warp * 2 + slot) * kSlot + lane, false);
+        for (int w = warp + 1; w < kGemvWarps; ++w)
+            for (int s2 = 0; s2 < 2; ++s2)
+                if (seg_unit[w][s2] == unit) add_acc<NT>(acc, red + (w * 2 + s2) * kSlot + lane, false);
+        const long long ustart = unit * p.n_ks, uend = ustart + p.n_ks;
+        const int bl = (int)(unit / p.n_st);
+        const int st = (int)(unit - (long long)bl * p.n_st);
+        if (ustart >= clo && uend <= chi) {
+            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+            continue;
+        }
+        // crosses a CTA boundary: publish the CTA partial; last CTA reduces
+        const int first = owner_of(ustart, total, NC);
+        const int last = owner_of(uend - 1, total, NC);
+        const int gslot = (c == first) ? 1 : 0;
+        store_acc<NT>(p.partial + ((long long)c * 2 + gslot) * kSlot + lane, acc, true);
+        __threadfence();
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev != last - first) continue;
+        __threadfence();
+        zero_acc<NT>(acc);
+        for (int j = first; j <= last; ++j)
+            add_acc<NT>(acc, p.partial + ((long long)j * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
+        if (lane == 0) p.counters[unit] = 0;
         gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
     }
+    (void)s_last;
 }
 
 }  // namespace cascade

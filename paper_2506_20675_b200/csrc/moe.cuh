@@ -1,21 +1,23 @@
-// moe.cuh — router, expert union and expert combine (SURVEY.md §8(a2)
-// stages K1/K2 and the epilogue of K3).
+// moe.cuh — step entry (embedding), router + expert union, expert combine
+// (SURVEY.md §8(a2) stages K1/K2 and the epilogue of K3).
 //
-// moe_route_kernel (grid = T CTAs, one per in-flight token):
-//   1. RMSNorm of the residual row -> bf16 MoE input, written in B-frag
-//      layout for the expert GEMVs.
-//   2. Router logits (E routed rows, plus the Qwen shared-expert gate row)
-//      from the bf16 input and bf16 router weights, fp32 accumulate.
+// moe_route_kernel (grid = T tokens x router-row groups):
+//   1. RMSNorm of the residual row -> bf16 MoE input (B-frag layout for the
+//      expert GEMVs; written by the row-group-0 CTA of each token).
+//   2. Router logits: one warp per router row (E routed rows + the Qwen
+//      shared-expert gate row), bf16 weights, fp32 accumulate, all of a
+//      lane's 16-byte loads issued before any FMA.
 //   3. The last CTA to finish (atomic ticket) routes every token: softmax,
-//      top-k (ties -> lower expert index), gate weights (renormalised for
-//      Mixtral), then the expert union: OR of per-token masks, ascending
-//      unique-expert list, per-expert token ranks.  This is the real
-//      counterpart of the reference's stand-ins draw_expert_set /
-//      sample_active_experts (expert_model.hpp:100-139): union = distinct
-//      routed experts, shared blocks always active on top.
+//      top-k (larger logit first, lower expert index on ties), gate weights
+//      (renormalised over the k for Mixtral), then the expert union: OR of
+//      per-token 128-bit masks, ascending unique-expert list, per-expert
+//      token ranks.  This is the real counterpart of the reference's
+//      stand-ins draw_expert_set / sample_active_experts
+//      (expert_model.hpp:100-139): union = distinct routed experts, shared
+//      blocks always active on top.
 // moe_combine_kernel (grid = T): residual += sum_r w[t][r] * Y[t][r]
-//   (+ shared-gate * sum_b Y[t][k+b]) in fixed order, then the next
-//   RMSNorm (next layer's attention input, or the final norm).
+//   (+ shared-gate * sum_b Y[t][k+b]) in fixed order, then the next RMSNorm
+//   (next layer's attention input, or the final norm).
 #pragma once
 
 #include "common.cuh"
@@ -23,8 +25,23 @@
 namespace cascade {
 
 constexpr int kRouteThreads = 256;
-constexpr int kMaxExperts = 128;   // expert_model.hpp:96 (kMaxRoutedExperts)
+constexpr int kRouteWarps = kRouteThreads / 32;
+constexpr int kMaxExperts = 128;  // expert_model.hpp:96 (kMaxRoutedExperts)
 constexpr int kMaxTopK = 16;
+
+// 1/rms of one fp32 row (d % 4 == 0), block-wide.
+__device__ __forceinline__ float row_rinv(const float* x, int d, float eps, float* red) {
+    float ss = 0.f;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const int n4 = d >> 2;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 v = x4[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    ss = block_sum(ss, red);
+    return 1.0f / sqrtf(ss / (float)d + eps);
+}
 
 struct RouteParams {
     const float* x;              // residual [T][d]
@@ -51,60 +68,78 @@ struct RouteParams {
 };
 
 __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p) {
+    griddep_wait();
+    griddep_launch();
     __shared__ float red[32];
     __shared__ int s_last;
+    __shared__ unsigned long long masks[kMaxT][2];
     extern __shared__ float xs[];  // [d] normalised input (bf16 values as fp32)
     const int t = blockIdx.x;
-    if (t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    const int grp = blockIdx.y;
+    if (t == 0 && grp == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
     const float* x = p.x + (long long)t * p.d;
-    float ss = 0.f;
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) ss += x[i] * x[i];
-    ss = block_sum(ss, red);
-    const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
+    const float rinv = row_rinv(x, p.d, p.eps, red);
     for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        const float v = (x[i] * rinv) * bits_to_f32(p.norm_w[i]);
-        const uint16_t b = bf16_bits(v);
-        p.xn_bfrag[bfrag_index(t, i)] = b;
-        if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
+        const uint16_t b = bf16_bits((x[i] * rinv) * bits_to_f32(p.norm_w[i]));
         xs[i] = bits_to_f32(b);
+        if (grp == 0) {
+            p.xn_bfrag[bfrag_index(t, i)] = b;
+            if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
+        }
     }
     __syncthreads();
     const int n_rows = p.E + (p.shared_gate ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int e = warp; e < n_rows; e += kRouteThreads / 32) {
-        const uint32_t* w2 = reinterpret_cast<const uint32_t*>(p.router_w + (long long)e * p.d);
+    const int e = grp * kRouteWarps + warp;
+    if (e < n_rows) {
+        const uint4* w4 = reinterpret_cast<const uint4*>(p.router_w + (long long)e * p.d);
+        const int n8 = p.d >> 3;  // uint4 per row
         float acc = 0.f;
-        for (int i = lane; i < p.d / 2; i += 32) {
-            const uint32_t ww = __ldg(w2 + i);
-            acc = fmaf(xs[2 * i], __uint_as_float(ww << 16), acc);
-            acc = fmaf(xs[2 * i + 1], __uint_as_float(ww & 0xFFFF0000u), acc);
+        for (int base = 0; base < n8; base += 32 * 8) {
+            uint4 w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = base + u * 32 + lane;
+                w[u] = i < n8 ? __ldg(w4 + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = base + u * 32 + lane;
+                if (i >= n8) continue;
+                const float* xv = xs + i * 8;
+                const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc = fmaf(xv[2 * q], __uint_as_float(ww[q] << 16), acc);
+                    acc = fmaf(xv[2 * q + 1], __uint_as_float(ww[q] & 0xFFFF0000u), acc);
+                }
+            }
         }
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) p.logits[t * (p.E + 1) + e] = acc;
     }
-    if (p.zero_nonlocal) {
+    if (p.zero_nonlocal && grp == 0) {
         // EP: every (token, rank) row is written by exactly one rank's down
         // GEMV; the others must contribute exact zeros to the all-reduce.
-        float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d;
-        for (int i = threadIdx.x; i < (p.k + p.S) * p.d; i += blockDim.x) y[i] = 0.f;
+        float4* y = reinterpret_cast<float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
+        for (int i = threadIdx.x; i < (p.k + p.S) * p.d / 4; i += blockDim.x) y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1) == p.T - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1) == (int)(gridDim.x * gridDim.y) - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
 
     // ---- routing of all tokens (last CTA) ----
-    __shared__ unsigned long long masks[kMaxT][2];
-    for (int tt = warp; tt < p.T; tt += kRouteThreads / 32) {
+    for (int tt = warp; tt < p.T; tt += kRouteWarps) {
         const float* lg = p.logits + tt * (p.E + 1);
         float v[kMaxExperts / 32];
         float m = -INFINITY;
 #pragma unroll
         for (int q = 0; q < kMaxExperts / 32; ++q) {
-            const int e = lane + 32 * q;
-            v[q] = e < p.E ? __ldcg(lg + e) : -INFINITY;
+            const int ei = lane + 32 * q;
+            v[q] = ei < p.E ? __ldcg(lg + ei) : -INFINITY;
             m = fmaxf(m, v[q]);
         }
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -117,15 +152,14 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
         float chosen_e[kMaxTopK];
         int chosen_i[kMaxTopK];
         for (int r = 0; r < p.k; ++r) {
-            // warp argmax: larger logit first, lower index on ties
             float bv = -INFINITY;
             int bi = 0x7fffffff;
 #pragma unroll
             for (int q = 0; q < kMaxExperts / 32; ++q) {
-                const int e = lane + 32 * q;
-                if (e < p.E && (v[q] > bv || (v[q] == bv && e < bi))) {
+                const int ei = lane + 32 * q;
+                if (ei < p.E && (v[q] > bv || (v[q] == bv && ei < bi))) {
                     bv = v[q];
-                    bi = e;
+                    bi = ei;
                 }
             }
             for (int o = 16; o > 0; o >>= 1) {
@@ -168,15 +202,15 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
         }
         *p.union_size = __popcll(u0) + __popcll(u1);
         int n = 0;
-        for (int e = p.e_lo; e < p.e_hi; ++e) {
-            const bool on = e < 64 ? ((u0 >> e) & 1ull) : ((u1 >> (e - 64)) & 1ull);
+        for (int ei = p.e_lo; ei < p.e_hi; ++ei) {
+            const bool on = ei < 64 ? ((u0 >> ei) & 1ull) : ((u1 >> (ei - 64)) & 1ull);
             if (!on) continue;
-            p.list[n] = e - p.e_lo;
+            p.list[n] = ei - p.e_lo;
             for (int tt = 0; tt < kMaxT; ++tt) {
                 int rank = -1;
                 if (tt < p.T)
                     for (int r = 0; r < p.k; ++r)
-                        if (p.topk_id[tt * p.k + r] == e) rank = r;
+                        if (p.topk_id[tt * p.k + r] == ei) rank = r;
                 p.route_rank[n * kMaxT + tt] = rank;
             }
             ++n;
@@ -210,38 +244,71 @@ struct CombineParams {
 };
 
 __global__ void __launch_bounds__(kRouteThreads) moe_combine_kernel(CombineParams p) {
+    griddep_wait();
+    griddep_launch();
     __shared__ float red[32];
+    __shared__ float wsh[kMaxTopK + 1];
     const int t = blockIdx.x;
-    float* x = p.x + (long long)t * p.d;
-    const float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d;
-    const float g = p.gsh[t];
-    float w[kMaxTopK];
-    for (int r = 0; r < p.k; ++r) w[r] = p.topk_w[t * p.k + r];
+    if (threadIdx.x < p.k) wsh[threadIdx.x] = p.topk_w[t * p.k + threadIdx.x];
+    if (threadIdx.x == 0) wsh[kMaxTopK] = p.gsh[t];
+    __syncthreads();
+    float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
+    const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
+    const int n4 = p.d >> 2;
+    const float g = wsh[kMaxTopK];
     float ss = 0.f;
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        float acc = 0.f;
-        for (int r = 0; r < p.k; ++r) acc += w[r] * y[(long long)r * p.d + i];
-        if (p.S > 0) {
-            float sh = 0.f;
-            for (int b = 0; b < p.S; ++b) sh += y[(long long)(p.k + b) * p.d + i];
-            acc += g * sh;
+#pragma unroll 2
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < p.k; ++r) {
+            const float4 y = y4[(long long)r * n4 + i];
+            const float w = wsh[r];
+            acc.x += w * y.x;
+            acc.y += w * y.y;
+            acc.z += w * y.z;
+            acc.w += w * y.w;
         }
-        if (p.tap_moe) p.tap_moe[(long long)t * p.d + i] = acc;
-        const float nx = x[i] + acc;
-        x[i] = nx;
-        if (p.tap_x) p.tap_x[(long long)t * p.d + i] = nx;
-        ss += nx * nx;
+        if (p.S > 0) {
+            float4 sh = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int b = 0; b < p.S; ++b) {
+                const float4 y = y4[(long long)(p.k + b) * n4 + i];
+                sh.x += y.x;
+                sh.y += y.y;
+                sh.z += y.z;
+                sh.w += y.w;
+            }
+            acc.x += g * sh.x;
+            acc.y += g * sh.y;
+            acc.z += g * sh.z;
+            acc.w += g * sh.w;
+        }
+        if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
+        float4 nx = x4[i];
+        nx.x += acc.x;
+        nx.y += acc.y;
+        nx.z += acc.z;
+        nx.w += acc.w;
+        x4[i] = nx;
+        if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = nx;
+        ss += nx.x * nx.x + nx.y * nx.y + nx.z * nx.z + nx.w * nx.w;
     }
     ss = block_sum(ss, red);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        const uint16_t b = bf16_bits((x[i] * rinv) * bits_to_f32(p.norm_w[i]));
-        p.xn_bfrag[bfrag_index(t, i)] = b;
-        if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+        const float4 v = x4[i];
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * i + q;
+            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[col]));
+            p.xn_bfrag[bfrag_index(t, col)] = b;
+            if (p.tap_xn) p.tap_xn[(long long)t * p.d + col] = b;
+        }
     }
 }
 
-// Step entry: token embedding + first RMSNorm; stamps the step start.
+// Step entry: token embedding + first RMSNorm + the step's RoPE table;
+// stamps the step start.
 struct StepParams {            // H2D-copied at the head of every step graph
     int32_t mode;              // 0 verify (row 0 = pending token), 1 prefill (all given)
     int32_t commit;            // 1: advance the cache; 0: re-verify the same context
@@ -267,19 +334,31 @@ struct EmbedParams {
     float* x;                    // out residual [T][d]
     uint16_t* xn_bfrag;          // out
     int* tokens_used;            // out [T]
+    float2* rope;                // out [T][hd/2] (cos, sin) at position ctx + t
     unsigned long long* stamp;   // step start
     float* tap_x;                // optional
     uint16_t* tap_xn;            // optional
-    int T, d;
+    int T, d, hd;
+    double rope_theta;
     float eps;
 };
 
 __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p) {
+    griddep_wait();
+    griddep_launch();
     __shared__ float red[32];
     const int t = blockIdx.x;
     if (t == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
     const int tok = (p.sp->mode == 0 && t == 0) ? p.st->pending : p.sp->tokens[t];
     if (threadIdx.x == 0) p.tokens_used[t] = tok;
+    const int pos = p.st->cache_len + t;
+    for (int i = threadIdx.x; i < p.hd / 2; i += blockDim.x) {
+        // angle in fp64: exact to fp32 rounding at any context length
+        const double inv = pow(p.rope_theta, -2.0 * (double)i / (double)p.hd);
+        double sn, cs;
+        sincos((double)pos * inv, &sn, &cs);
+        p.rope[t * (p.hd / 2) + i] = make_float2((float)cs, (float)sn);
+    }
     const uint16_t* e = p.embed + (long long)tok * p.d;
     float* x = p.x + (long long)t * p.d;
     float ss = 0.f;

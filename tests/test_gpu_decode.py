@@ -1,0 +1,125 @@
+"""GPU tests of the full speculative decode loop (cascade_decode): n-gram
+drafter -> device verification step -> utility analyzer -> test-and-set
+controller, all in host C++ over the C ABI (BASELINE config 1 and 4).
+
+* Greedy speculative decoding is lossless: for every policy the emitted
+  tokens equal the target's greedy continuation (checked against the CPU
+  oracle's K=0 decode).
+* K-decision traces: with an injected k -> time cost (real device
+  acceptance), the controller's K trace is replayed through the reference
+  controller (oracle/_ref, the unmodified specsim headers) and through this
+  repository's headers; all three must agree exactly.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2506_20675_b200 as cb
+from oracle.oracle import OracleModel, OracleSession
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import specsim_shim as sh  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    shape = cb.preset("tiny")
+    m = cb.Model(shape, cb.TINY_SEED)
+    s = cb.Session(m, max_ctx=1024, k_max=15)
+    yield shape, m, s
+    s.close()
+    m.close()
+
+
+def repetitive_prompt(n=64, seed=1):
+    rng = np.random.default_rng(seed)
+    motif = rng.integers(0, 1024, 9)
+    return np.concatenate([np.tile(motif, n // 9 + 1)[:n - 7], rng.integers(0, 1024, 7)]).astype(np.int32)
+
+
+def oracle_greedy(shape, prompt, n):
+    om = OracleModel(shape, cb.TINY_SEED)
+    os_ = OracleSession(om, 1024)
+    os_.prefill(prompt)
+    out, margins = [], []
+    for _ in range(n):
+        acc, am, lg, mg, us = os_.verify([])
+        out.append(int(am[0]))
+        margins.append(float(mg[0]))
+    return out, margins
+
+
+def agree_prefix(a, b):
+    n = 0
+    for x, y in zip(a, b):
+        if x != y:
+            break
+        n += 1
+    return n
+
+
+@pytest.mark.parametrize("policy", [0, 1, 3, 8, -1])
+def test_speculative_decode_is_lossless(tiny, policy):
+    shape, m, s = tiny
+    prompt = repetitive_prompt()
+    N = 96
+    truth, margins = oracle_greedy(shape, prompt, N)
+    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=policy, max_new=N, ngram_n=3), telemetry_cap=512)
+    assert len(toks) >= N
+    n = agree_prefix(toks[:N], truth)
+    if n < N:
+        # only a near-tie of the target's own argmax may split the decodes
+        assert margins[n] < 5e-2, (policy, n, margins[n])
+    # IterationRecord invariants (utility.hpp:89-91)
+    k_used, emitted, k_off = tel[:, 1], tel[:, 2], tel[:, 9]
+    assert np.all(emitted >= 1) and np.all(emitted <= k_used + 1)
+    assert np.all(k_off <= k_used)
+    assert int(emitted.sum()) == len(toks)
+    if policy > 0:
+        # the n-gram drafter finds the motif: some drafts are accepted
+        assert (emitted > 1).any()
+        assert tel[:, 9].max() <= policy
+
+
+def test_utility_identity_from_device_telemetry(tiny):
+    """run_utility * TPOT == t_base (utility.hpp:56-76) on device-measured
+    iteration times: the Theorem-1 identity of the paper."""
+    shape, m, s = tiny
+    toks, tel, n_it = s.decode(repetitive_prompt(seed=3), cb.decode_cfg(policy=-1, max_new=200), telemetry_cap=1024)
+    probes = tel[tel[:, 7] == 0]
+    t_base = probes[:4, 6].mean()
+    tokens, iters, time = tel[:, 2].sum(), len(tel), tel[:, 6].sum()
+    u = (tokens / iters) / ((time / iters) / t_base)
+    tpot = time / tokens
+    assert abs(u * tpot - t_base) / t_base < 1e-12
+    assert np.all(tel[:, 6] > 0)  # device-measured ns
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_k_trace_matches_reference_controller(tiny, seed):
+    """Injected cost model: iteration time = cost_by_k[k]; acceptance is the
+    real greedy acceptance of the device.  The K decisions must equal the
+    reference controller's on the same record stream."""
+    shape, m, s = tiny
+    costs = [1.0, 1.35, 1.6, 1.8, 2.3, 2.6, 2.9, 3.2] + [4.0] * 8
+    cfgd = dict(k_max=5, k_start=3, t_trial=4, max_trials=4, s_set=16)
+    dc = cb.decode_cfg(policy=-1, max_new=300, ngram_n=2, cost_by_k=costs, **cfgd)
+    toks, tel, n_it = s.decode(repetitive_prompt(seed=seed), dc, telemetry_cap=2048)
+    assert n_it == len(tel)
+    c = sh.cfg(k_max=5, k_start=3)
+    tokens = tel[:, 2].astype(np.int32)
+    totals = tel[:, 6]
+    assert np.array_equal(totals, np.array([costs[int(k)] for k in tel[:, 1]]))
+    for which in ("ref", "ours"):
+        if not sh.available(which):
+            pytest.skip(f"{which} controller build missing")
+        k_ref, tag_ref = sh.Shim(which).controller_replay(c, tokens, totals)
+        assert np.array_equal(k_ref, tel[:, 1].astype(np.int32)), which
+        assert np.array_equal(tag_ref, tel[:, 7].astype(np.int32)), which
+    # the controller actually explored: probes, tests and sets all occur
+    assert set(tel[:, 7].astype(int)) == {0, 1, 2}

@@ -1,0 +1,102 @@
+"""GPU parity at the BASELINE model widths (Mixtral-8x7B, OLMoE-1B-7B,
+Qwen1.5-MoE-A2.7B) with the layer count reduced so the CPU oracle finishes
+in seconds.  Each layer is checked teacher-forced (the oracle is fed the
+device's stage inputs): router top-k exact (margin-flagged), expert union
+exact, MoE / attention outputs and logits within tolerance; greedy argmax
+and acceptance exact unless flagged.  Full-depth, full-size properties are
+in test_gpu_fullsize.py.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2506_20675_b200 as cb
+from oracle.oracle import OracleModel, greedy_accept, union
+
+pytestmark = pytest.mark.gpu
+
+ROUTER_MARGIN = 1e-3   # router decisions closer than this (logit units) are flagged
+OUT_RTOL = 1e-2        # of max |oracle|
+OUT_ATOL = 1e-3
+
+
+def run_teacher_forced(name, layers, K, ctx=200, seed=7):
+    shape = cb.preset(name).with_layers(layers)
+    m = cb.Model(shape, seed)
+    om = OracleModel(shape, seed)
+    s = cb.Session(m, max_ctx=ctx + 32, k_max=15)
+    rng = np.random.default_rng(seed)
+    s.prefill(rng.integers(0, shape.vocab, ctx + 1).astype(np.int32))
+    s.enable_taps(True)
+    drafts = rng.integers(0, shape.vocab, K).astype(np.int32)
+    out = s.verify(drafts)
+    T = K + 1
+    x_in, x_mid = s.tap("x_in"), s.tap("x_mid")
+    xn_moe = s.tap("xn_moe")
+    rl, tid, tw, moe = s.tap("router_logits"), s.tap("topk_id"), s.tap("topk_w"), s.tap("moe_out")
+    flagged = 0
+    E, k = shape.experts_per_layer, shape.top_k
+    stats = {}
+    for l in range(layers):
+        kc = s.read_kv(l, 0, ctx)
+        vc = s.read_kv(l, 1, ctx)
+        oa, kn, vn = om.attention(l, x_in[l, :T], ctx, kc, vc)
+        ga = x_mid[l, :T].astype(np.float64) - x_in[l, :T]
+        stats[f"attn_err_l{l}"] = float(np.abs(ga - oa).max() / np.abs(oa).max())
+        assert np.abs(ga - oa).max() <= OUT_ATOL + OUT_RTOL * np.abs(oa).max(), (l, stats)
+        logits, topk, topw, gsh, margin = om.router(l, xn_moe[l, :T])
+        assert np.abs(rl[l, :T, :E] - logits[:, :E]).max() <= 1e-4 * max(1.0, np.abs(logits[:, :E]).max())
+        if shape.shared_gate:
+            assert np.abs(rl[l, :T, E] - logits[:, E]).max() <= 1e-4 * max(1.0, np.abs(logits[:, E]).max())
+        ok_rows = margin >= ROUTER_MARGIN
+        flagged += int((~ok_rows).sum())
+        assert np.array_equal(tid[l, :T][ok_rows], topk[ok_rows]), l
+        assert np.allclose(tw[l, :T][ok_rows], topw[ok_rows], rtol=2e-5, atol=1e-6)
+        u_dev = s.union_sizes()[l] if layers == 1 else None
+        assert sorted(set(tid[l, :T].ravel().tolist())) == union(tid[l, :T]).tolist()
+        om_out = om.moe(l, xn_moe[l, :T], tid[l, :T], tw[l, :T].astype(np.float64), gsh)
+        stats[f"moe_err_l{l}"] = float(np.abs(moe[l, :T] - om_out).max() / np.abs(om_out).max())
+        assert np.abs(moe[l, :T] - om_out).max() <= OUT_ATOL + OUT_RTOL * np.abs(om_out).max(), (l, stats)
+        om.drop_cache()
+    x_last = (x_mid[-1, :T].astype(np.float64) + moe[-1, :T]).astype(np.float32)
+    xf = om.rmsnorm(cb.T_FINAL_NORM, 0, x_last)
+    lg, am, mg = om.lm_head(xf)
+    glog = s.tap("final_logits")[:T]
+    err = float(np.abs(glog - lg).max())
+    stats["logit_err"] = err
+    assert err <= 2e-3 + 1e-2 * np.abs(lg).max()
+    for t in range(T):
+        if mg[t] > 2 * err:
+            assert out.argmax[t] == am[t]
+    acc, _ = greedy_accept(np.array(out.argmax[:T]), drafts)
+    assert out.accepted == acc
+    assert flagged <= max(1, T * layers // 10)
+    us = s.union_sizes()
+    for l in range(layers):
+        assert us[l] == len(union(tid[l, :T]))
+    s.close()
+    m.close()
+    return stats
+
+
+def test_mixtral_width_K3():
+    st = run_teacher_forced("mixtral", 2, 3)
+    print(st)
+
+
+def test_mixtral_width_K8():
+    st = run_teacher_forced("mixtral", 1, 8)
+    print(st)
+
+
+@pytest.mark.parametrize("K", [0, 8])
+def test_olmoe_width(K):
+    st = run_teacher_forced("olmoe", 2, K)
+    print(st)
+
+
+@pytest.mark.parametrize("K", [0, 5])
+def test_qwen15_width_shared_experts(K):
+    """Shared expert as 4 always-active blocks with the sigmoid gate."""
+    st = run_teacher_forced("qwen15", 2, K)
+    print(st)
