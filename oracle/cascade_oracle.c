@@ -590,6 +590,7 @@ struct orc_session {
     int max_ctx, len, pending;
     uint16_t* kc; /* [L][KV][max_ctx][hd] */
     uint16_t* vc;
+    double min_router_margin; /* smallest router decision gap seen (flags near-ties) */
 };
 
 orc_session* orc_session_create(orc_model* m, int max_ctx) {
@@ -600,6 +601,7 @@ orc_session* orc_session_create(orc_model* m, int max_ctx) {
     const size_t n = (size_t)m->L * m->KV * s->max_ctx * m->hd;
     s->kc = (uint16_t*)calloc(n, 2);
     s->vc = (uint16_t*)calloc(n, 2);
+    s->min_router_margin = INFINITY;
     return s;
 }
 
@@ -611,6 +613,13 @@ void orc_session_destroy(orc_session* s) {
 }
 
 int orc_cache_len(const orc_session* s) { return s ? s->len : -1; }
+
+double orc_min_router_margin(orc_session* s, int reset) {
+    if (!s) return -1.0;
+    const double v = s->min_router_margin;
+    if (reset) s->min_router_margin = INFINITY;
+    return v;
+}
 
 /* forward T tokens at positions len..len+T-1; writes their KV rows; logits
  * [T][V] of the final norm output */
@@ -629,6 +638,7 @@ static int forward(orc_session* s, const int32_t* toks, int T, double* logits, i
     int32_t* topk = (int32_t*)malloc((size_t)T * m->k * sizeof(int32_t));
     double* topw = (double*)malloc((size_t)T * m->k * sizeof(double));
     double* gsh = (double*)malloc((size_t)T * sizeof(double));
+    double* rmg = (double*)malloc((size_t)T * sizeof(double));
     for (int l = 0; l < m->L; ++l) {
         uint16_t* kc = s->kc + (size_t)l * KV * s->max_ctx * hd;
         uint16_t* vc = s->vc + (size_t)l * KV * s->max_ctx * hd;
@@ -640,7 +650,9 @@ static int forward(orc_session* s, const int32_t* toks, int T, double* logits, i
             }
         for (long i = 0; i < (long)T * d; ++i) x[i] += a[i];
         rmsnorm_d(m, W(m, CASCADE_T_FFN_NORM, l, 0), x, T, xn);
-        orc_router(m, l, xn, T, NULL, topk, topw, gsh, NULL);
+        orc_router(m, l, xn, T, NULL, topk, topw, gsh, rmg);
+        for (int t = 0; t < T; ++t)
+            if (rmg[t] < s->min_router_margin) s->min_router_margin = rmg[t];
         if (union_sizes) union_sizes[l] = orc_union(topk, T, m->k, NULL);
         orc_moe(m, l, xn, T, topk, topw, gsh, a);
         for (long i = 0; i < (long)T * d; ++i) x[i] += a[i];
@@ -651,6 +663,7 @@ static int forward(orc_session* s, const int32_t* toks, int T, double* logits, i
         linear(m, W(m, CASCADE_T_LM_HEAD, 0, 0), m->V, d, xx, T, logits);
         free(xx);
     }
+    free(rmg);
     free(gsh);
     free(topw);
     free(topk);

@@ -76,6 +76,9 @@ int orc_prefill(orc_session* s, const int32_t* prompt, int n);
 int orc_verify(orc_session* s, const int32_t* drafts, int K, double* logits, int32_t* argmax,
                double* margin, int32_t* union_sizes);
 int orc_cache_len(const orc_session* s);
+/* smallest router top-k decision margin (logit units) seen since the last
+ * reset: a device/oracle routing disagreement below it is a flagged tie */
+double orc_min_router_margin(orc_session* s, int reset);
 
 #ifdef __cplusplus
 }

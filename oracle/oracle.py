@@ -50,6 +50,7 @@ def lib():
             "orc_prefill": (c, [P, I32P, c]),
             "orc_verify": (c, [P, I32P, c, DP, I32P, DP, I32P]),
             "orc_cache_len": (c, [P]),
+            "orc_min_router_margin": (ctypes.c_double, [P, c]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -202,6 +203,9 @@ class OracleSession:
         acc = _chk(lib().orc_verify(self.h, _p(d, ctypes.c_int32) if K else None, K, _p(logits, ctypes.c_double),
                                     _p(am, ctypes.c_int32), _p(mg, ctypes.c_double), _p(us, ctypes.c_int32)))
         return acc, am, logits, mg, us
+
+    def min_router_margin(self, reset=True):
+        return lib().orc_min_router_margin(self.h, 1 if reset else 0)
 
     @property
     def cache_len(self):

@@ -43,15 +43,19 @@ def repetitive_prompt(n=64, seed=1):
 
 
 def oracle_greedy(shape, prompt, n):
+    """Oracle K=0 decode; flagged[i] marks a near-tie at or before token i
+    (router gap < 1e-2 anywhere, prefill included, or LM top-2 gap < 5e-2)."""
     om = OracleModel(shape, cb.TINY_SEED)
     os_ = OracleSession(om, 1024)
     os_.prefill(prompt)
-    out, margins = [], []
+    bad = os_.min_router_margin() < 1e-2
+    out, flagged = [], []
     for _ in range(n):
         acc, am, lg, mg, us = os_.verify([])
+        bad = bad or os_.min_router_margin() < 1e-2 or mg[0] < 5e-2
         out.append(int(am[0]))
-        margins.append(float(mg[0]))
-    return out, margins
+        flagged.append(bad)
+    return out, flagged
 
 
 def agree_prefix(a, b):
@@ -63,18 +67,29 @@ def agree_prefix(a, b):
     return n
 
 
-@pytest.mark.parametrize("policy", [0, 1, 3, 8, -1])
-def test_speculative_decode_is_lossless(tiny, policy):
+def test_k0_decode_matches_oracle_greedy(tiny):
     shape, m, s = tiny
     prompt = repetitive_prompt()
     N = 96
-    truth, margins = oracle_greedy(shape, prompt, N)
-    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=policy, max_new=N, ngram_n=3), telemetry_cap=512)
-    assert len(toks) >= N
+    truth, flagged = oracle_greedy(shape, prompt, N)
+    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=0, max_new=N), telemetry_cap=512)
     n = agree_prefix(toks[:N], truth)
     if n < N:
-        # only a near-tie of the target's own argmax may split the decodes
-        assert margins[n] < 5e-2, (policy, n, margins[n])
+        assert flagged[n], n  # only a flagged near-tie may split device and oracle
+
+
+@pytest.mark.parametrize("policy", [1, 3, 8, -1])
+def test_speculative_decode_is_lossless(tiny, policy):
+    """Every policy emits the K=0 greedy sequence of the same device (the
+    step's fp32 summation order varies with T, so only exact ties could
+    split them)."""
+    shape, m, s = tiny
+    prompt = repetitive_prompt()
+    N = 96
+    ref, _, _ = s.decode(prompt, cb.decode_cfg(policy=0, max_new=N), telemetry_cap=512)
+    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=policy, max_new=N, ngram_n=3), telemetry_cap=512)
+    assert len(toks) >= N
+    assert agree_prefix(toks[:N], ref[:N]) == N, (policy, list(toks[:N]), list(ref[:N]))
     # IterationRecord invariants (utility.hpp:89-91)
     k_used, emitted, k_off = tel[:, 1], tel[:, 2], tel[:, 9]
     assert np.all(emitted >= 1) and np.all(emitted <= k_used + 1)

@@ -138,51 +138,63 @@ def greedy_sequence(om, p, n):
     return seq
 
 
+ROUTER_FLAG = 1e-2  # router decision gaps below this (logit units) are flagged near-ties
+
+
 @pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
 def test_end_to_end_greedy_decode(tiny, K):
     """Lock-step decode, device vs independent oracle (no teacher forcing):
     drafts are the true greedy continuation with random corruptions, so
     every accepted count 0..K occurs.  Logits must agree within the stated
     tolerance; argmax rows, accepted counts, KV length and per-layer union
-    sizes must agree exactly unless the oracle's top-2 margin is inside the
-    observed logit error (flagged near-tie: the decodes may then diverge)."""
+    sizes must agree exactly.  A comparison stops at the first flagged
+    near-tie (an oracle router decision gap < ROUTER_FLAG anywhere, prefill
+    included, or an LM top-2 gap inside the observed logit error), after
+    which the two decodes may legitimately diverge; several prompts are
+    tried so that enough clean lock-step verifies are compared."""
     shape, m, om = tiny
-    p = prompt(40, seed=10 + K)
-    truth = greedy_sequence(om, p, 80)
-    s = cb.Session(m, max_ctx=512, k_max=8)
-    s.enable_taps(True)  # eager path + final logits tap
-    s.prefill(p)
-    os_ = OracleSession(om, 512)
-    os_.prefill(p)
-    rng = np.random.default_rng(K)
-    pos = 0  # index into truth of the next token to be emitted
-    steps = 0
+    clean_steps = 0
     worst = 0.0
-    while pos + K < len(truth) and steps < 30:
-        drafts = np.array(truth[pos: pos + K], np.int32)
-        for i in range(K):
-            if rng.random() < 0.3:
-                drafts[i] = rng.integers(0, shape.vocab)
-        g = s.verify(drafts)
-        acc, am, lg, mg, us = os_.verify(drafts)
-        T = K + 1
-        glog = s.tap("final_logits")[:T]
-        err = float(np.abs(glog - lg).max())
-        worst = max(worst, err)
-        assert err <= LOGIT_ATOL + LOGIT_RTOL * np.abs(lg).max(), (steps, err)
-        if np.any(mg[:T] <= 2 * err + MARGIN):
-            break  # flagged near-tie
-        assert list(g.argmax[:T]) == list(am), steps
-        assert g.accepted == acc
-        assert g.emitted == acc + 1
-        assert g.cache_len == os_.cache_len
-        assert list(s.union_sizes()) == list(us)
-        assert list(g.tokens[: acc + 1]) == list(truth[pos: pos + acc + 1])
-        pos += acc + 1
-        steps += 1
-    print(f"K={K}: {steps} lock-step verifies, worst |dlogit| = {worst:.2e}")
-    assert steps >= 8
-    s.close()
+    for trial in range(8):
+        p = prompt(24, seed=100 * K + trial)
+        truth = greedy_sequence(om, p, 60)
+        s = cb.Session(m, max_ctx=512, k_max=8)
+        s.enable_taps(True)  # eager path + final logits tap
+        s.prefill(p)
+        os_ = OracleSession(om, 512)
+        os_.prefill(p)
+        if os_.min_router_margin() < ROUTER_FLAG:
+            s.close()
+            continue
+        rng = np.random.default_rng(K + trial)
+        pos = 0
+        while pos + K < len(truth):
+            drafts = np.array(truth[pos: pos + K], np.int32)
+            for i in range(K):
+                if rng.random() < 0.3:
+                    drafts[i] = rng.integers(0, shape.vocab)
+            g = s.verify(drafts)
+            acc, am, lg, mg, us = os_.verify(drafts)
+            if os_.min_router_margin() < ROUTER_FLAG:
+                break
+            T = K + 1
+            glog = s.tap("final_logits")[:T]
+            err = float(np.abs(glog - lg).max())
+            worst = max(worst, err)
+            assert err <= LOGIT_ATOL + LOGIT_RTOL * np.abs(lg).max(), (trial, pos, err)
+            if np.any(mg[:T] <= 2 * err + MARGIN):
+                break
+            assert list(g.argmax[:T]) == list(am), (trial, pos)
+            assert g.accepted == acc
+            assert g.emitted == acc + 1
+            assert g.cache_len == os_.cache_len
+            assert list(s.union_sizes()) == list(us)
+            assert list(g.tokens[: acc + 1]) == list(truth[pos: pos + acc + 1])
+            pos += acc + 1
+            clean_steps += 1
+        s.close()
+    print(f"K={K}: {clean_steps} clean lock-step verifies, worst |dlogit| = {worst:.2e}")
+    assert clean_steps >= 12
 
 
 def test_graph_replay_matches_eager(tiny):
