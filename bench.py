@@ -278,7 +278,7 @@ def run_ours(args, rank, world, local_rank):
         for n_, k_ in zip(ns, kind):
             cls[cb.KERNEL_CLASSES[k_]] = cls.get(cb.KERNEL_CLASSES[k_], 0.0) + float(n_)
         d, f = shape.d_model, shape.d_ff
-        eb = sum((u + shape.shared_experts) for u in us) * 3 * d * f * 2
+        eb = sum((int(u) + shape.shared_experts) for u in us) * 3 * d * f * 2
         et = cls.get("expert_gate_up", 0.0) + cls.get("expert_down", 0.0)
         exp_bytes += eb
         exp_ns += et

@@ -470,62 +470,51 @@ static int attention_d(orc_model* m, int layer, const double* xd, int T, int ctx
             }
         }
     }
-    /* Device precision contract (attention.cuh): q is rotated, scaled by
-     * 1/sqrt(hd) and rounded to bf16; keys are split into 64-key chunks of
-     * the cache plus one chunk of the T new tokens; inside a chunk the
-     * probabilities exp(s - m_chunk) enter P*V rounded to bf16 while the
-     * chunk sum uses them unrounded; chunks merge with the usual rescaling. */
+    /* Device precision contract (attention.cuh): K/V are bf16 in the cache,
+     * q and P enter the tensor cores as two-term (hi + lo) bf16 pairs, i.e.
+     * the softmax is fp32-accurate; the attention output is rounded to bf16
+     * for the O projection.  The oracle therefore computes an exact (fp64)
+     * softmax over the bf16 keys/values and rounds only the output. */
     const double scale = 1.0 / sqrt((double)hd);
     double* o = (double*)malloc((size_t)T * H * hd * sizeof(double));
-    double* qs = (double*)malloc((size_t)hd * sizeof(double));
-    double* sc = (double*)malloc(64 * sizeof(double));
-    double* oc = (double*)malloc((size_t)hd * sizeof(double));
-    const int nch = (ctx + 63) / 64;
+    double* sc = (double*)malloc((size_t)(ctx + T) * sizeof(double));
     for (int t = 0; t < T; ++t)
         for (int h = 0; h < H; ++h) {
             const int kvh = h / G;
             const double* qv = q + ((long)t * H + h) * hd;
-            for (int i = 0; i < hd; ++i) qs[i] = bf(d2bf(qv[i] * scale));
-            double M = -INFINITY, L = 0;
+            const int n = ctx + t + 1;
+            double mx = -INFINITY;
+            for (int j = 0; j < n; ++j) {
+                double s2 = 0;
+                if (j < ctx) {
+                    const uint16_t* kr = kc + ((long)kvh * kc_stride + j) * hd;
+                    for (int i = 0; i < hd; ++i) s2 += qv[i] * bf(kr[i]);
+                } else {
+                    const double* kr = kk + ((long)(j - ctx) * KV + kvh) * hd;
+                    for (int i = 0; i < hd; ++i) s2 += qv[i] * kr[i];
+                }
+                sc[j] = s2 * scale;
+                mx = sc[j] > mx ? sc[j] : mx;
+            }
+            double z = 0;
+            for (int j = 0; j < n; ++j) {
+                sc[j] = exp(sc[j] - mx);
+                z += sc[j];
+            }
             double* ov = o + ((long)t * H + h) * hd;
             for (int i = 0; i < hd; ++i) ov[i] = 0;
-            for (int c = 0; c <= nch; ++c) {
-                const int is_new = c == nch;
-                const int j0 = is_new ? 0 : c * 64;
-                const int nkeys = is_new ? t + 1 : ((ctx - j0) < 64 ? (ctx - j0) : 64);
-                double mc = -INFINITY;
-                for (int j = 0; j < nkeys; ++j) {
-                    const double* kn_ = is_new ? kk + ((long)j * KV + kvh) * hd : NULL;
-                    const uint16_t* kr = is_new ? NULL : kc + ((long)kvh * kc_stride + j0 + j) * hd;
-                    double s2 = 0;
-                    for (int i = 0; i < hd; ++i) s2 += qs[i] * (is_new ? kn_[i] : bf(kr[i]));
-                    sc[j] = s2;
-                    mc = s2 > mc ? s2 : mc;
+            for (int j = 0; j < n; ++j) {
+                const double pj = sc[j] / z;
+                if (j < ctx) {
+                    const uint16_t* vr = vc + ((long)kvh * kc_stride + j) * hd;
+                    for (int i = 0; i < hd; ++i) ov[i] += pj * bf(vr[i]);
+                } else {
+                    const double* vr = vv + ((long)(j - ctx) * KV + kvh) * hd;
+                    for (int i = 0; i < hd; ++i) ov[i] += pj * vr[i];
                 }
-                double lc = 0;
-                for (int i = 0; i < hd; ++i) oc[i] = 0;
-                for (int j = 0; j < nkeys; ++j) {
-                    const double e = exp(sc[j] - mc);
-                    lc += e;
-                    const double pb = bf(d2bf(e));
-                    const double* vn_ = is_new ? vv + ((long)j * KV + kvh) * hd : NULL;
-                    const uint16_t* vr = is_new ? NULL : vc + ((long)kvh * kc_stride + j0 + j) * hd;
-                    for (int i = 0; i < hd; ++i) oc[i] += pb * (is_new ? vn_[i] : bf(vr[i]));
-                }
-                if (mc > M) {
-                    const double r = exp(M - mc);
-                    L *= r;
-                    for (int i = 0; i < hd; ++i) ov[i] *= r;
-                    M = mc;
-                }
-                const double r = exp(mc - M);
-                L += lc * r;
-                for (int i = 0; i < hd; ++i) ov[i] += oc[i] * r;
             }
-            for (int i = 0; i < hd; ++i) ov[i] = bf(d2bf(ov[i] / L)); /* O-proj input is bf16 */
+            for (int i = 0; i < hd; ++i) ov[i] = bf(d2bf(ov[i])); /* O-proj input is bf16 */
         }
-    free(oc);
-    free(qs);
     linear(m, W(m, CASCADE_T_WO, layer, 0), d, H * hd, o, T, out);
     free(o);
     free(sc);

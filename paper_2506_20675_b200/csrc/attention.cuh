@@ -47,6 +47,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return (uint32_t)bf16_bits(lo) | ((uint32_t)bf16_bits(hi) << 16);
 }
 
+// hi/lo bf16 split of a pair: x ~= hi + lo with ~16 significant bits
+__device__ __forceinline__ void split_bf16x2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+    const uint16_t h0 = bf16_bits(x0), h1 = bf16_bits(x1);
+    hi = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    lo = (uint32_t)bf16_bits(x0 - bits_to_f32(h0)) | ((uint32_t)bf16_bits(x1 - bits_to_f32(h1)) << 16);
+}
+
 __device__ __forceinline__ void mma_bf16_regs(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                               uint32_t a3, uint32_t b0, uint32_t b1) {
     asm volatile(
@@ -58,11 +65,17 @@ __device__ __forceinline__ void mma_bf16_regs(float (&c)[4], uint32_t a0, uint32
 
 template <int HD>
 constexpr int attn_smem_bytes() {
-    return (kAttnMaxRows + 2 * kChunk) * (HD + 8) * 2;
+    return (2 * kAttnMaxRows + 2 * kChunk) * (HD + 8) * 2;
 }
 
+// Two-term bf16 operands.  q and P enter the tensor cores as hi + lo bf16
+// pairs (hi = bf16(x), lo = bf16(x - hi)), so QK^T and PV carry ~16
+// mantissa bits instead of 8: the attention result no longer depends on
+// which keys share a 64-key chunk (i.e. on T), and matches an fp32/fp64
+// softmax to ~1e-5.  K and V are bf16 in the cache, so they need one term.
+//
 // smem (bf16, row stride HD+8 -> conflict-free fragment loads):
-//   q [kAttnMaxRows][HD+8] | k [kChunk][HD+8] | v [kChunk][HD+8]
+//   q_hi [kAttnMaxRows][HD+8] | q_lo [..] | k [kChunk][HD+8] | v [kChunk][HD+8]
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
     griddep_wait();
@@ -73,7 +86,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
     constexpr int NDT = HD / 8;       // n8 dim tiles of PV
     extern __shared__ __align__(16) uint16_t sm[];
     uint16_t* qs = sm;
-    uint16_t* ks = qs + kAttnMaxRows * LD;
+    uint16_t* qsl = qs + kAttnMaxRows * LD;
+    uint16_t* ks = qsl + kAttnMaxRows * LD;
     uint16_t* vs = ks + kChunk * LD;
 
     const int G = p.H / p.KV;
@@ -107,8 +121,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 a *= p.scale;
                 b *= p.scale;
             }
-            qs[r * LD + i] = bf16_bits(a);
-            qs[r * LD + i + HALF] = bf16_bits(b);
+            const uint16_t ah = bf16_bits(a), bh = bf16_bits(b);
+            qs[r * LD + i] = ah;
+            qs[r * LD + i + HALF] = bh;
+            qsl[r * LD + i] = bf16_bits(a - bits_to_f32(ah));
+            qsl[r * LD + i + HALF] = bf16_bits(b - bits_to_f32(bh));
         }
         if (is_new) {
             for (int e = threadIdx.x; e < kChunk * HALF; e += blockDim.x) {
@@ -167,10 +184,15 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 const uint32_t a1 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0);
                 const uint32_t a2 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g) * LD + i0 + 8);
                 const uint32_t a3 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0 + 8);
+                const uint32_t l0 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g) * LD + i0);
+                const uint32_t l1 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g + 8) * LD + i0);
+                const uint32_t l2 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g) * LD + i0 + 8);
+                const uint32_t l3 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g + 8) * LD + i0 + 8);
 #pragma unroll
                 for (int n = 0; n < 8; ++n) {
                     const uint32_t b0 = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0);
                     const uint32_t b1 = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0 + 8);
+                    mma_bf16_regs(s[n], l0, l1, l2, l3, b0, b1);
                     mma_bf16_regs(s[n], a0, a1, a2, a3, b0, b1);
                 }
             }
@@ -218,10 +240,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 for (int q = 0; q < 4; ++q) o[n][q] = 0.f;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t a0 = pack_bf16x2(s[2 * kk][0], s[2 * kk][1]);
-                const uint32_t a1 = pack_bf16x2(s[2 * kk][2], s[2 * kk][3]);
-                const uint32_t a2 = pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-                const uint32_t a3 = pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3]);
+                uint32_t a0, a1, a2, a3, l0, l1, l2, l3;
+                split_bf16x2(s[2 * kk][0], s[2 * kk][1], a0, l0);
+                split_bf16x2(s[2 * kk][2], s[2 * kk][3], a1, l1);
+                split_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1], a2, l2);
+                split_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3], a3, l3);
 #pragma unroll
                 for (int n = 0; n < NDT; n += 2) {
                     // ldmatrix.x4.trans: lanes 0-15 -> rows of dims n*8, lanes 16-31 -> dims n*8+8
@@ -234,7 +257,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                         "ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
                         : "r"(addr));
+                    mma_bf16_regs(o[n], l0, l1, l2, l3, b0, b1);
                     mma_bf16_regs(o[n], a0, a1, a2, a3, b0, b1);
+                    mma_bf16_regs(o[n + 1], l0, l1, l2, l3, b2, b3);
                     mma_bf16_regs(o[n + 1], a0, a1, a2, a3, b2, b3);
                 }
             }

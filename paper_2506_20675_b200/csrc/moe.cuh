@@ -132,6 +132,8 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
     __threadfence();
 
     // ---- routing of all tokens (last CTA) ----
+    __shared__ int s_topk[kMaxT * kMaxTopK];
+    __shared__ int s_warp_on[kMaxExperts / 32];
     for (int tt = warp; tt < p.T; tt += kRouteWarps) {
         const float* lg = p.logits + tt * (p.E + 1);
         float v[kMaxExperts / 32];
@@ -149,8 +151,9 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
             if (lane + 32 * q < p.E) z += __expf(v[q] - m);
         for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
         unsigned long long m0 = 0, m1 = 0;
-        float chosen_e[kMaxTopK];
-        int chosen_i[kMaxTopK];
+        float zk = 0.f;
+        float my_e = 0.f;  // lane r keeps the r-th choice
+        int my_i = 0;
         for (int r = 0; r < p.k; ++r) {
             float bv = -INFINITY;
             int bi = 0x7fffffff;
@@ -173,54 +176,63 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
 #pragma unroll
             for (int q = 0; q < kMaxExperts / 32; ++q)
                 if (lane + 32 * q == bi) v[q] = -INFINITY;
-            chosen_e[r] = __expf(bv - m);
-            chosen_i[r] = bi;
+            const float ex = __expf(bv - m);
+            zk += ex;  // same order on every lane: r = 0..k-1
+            if (lane == r) {
+                my_e = ex;
+                my_i = bi;
+            }
             if (bi < 64) m0 |= 1ull << bi;
             else m1 |= 1ull << (bi - 64);
         }
+        const float den = p.renorm ? zk : z;
+        if (lane < p.k) {
+            s_topk[tt * p.k + lane] = my_i;
+            p.topk_id[tt * p.k + lane] = my_i;
+            p.topk_w[tt * p.k + lane] = my_e / den;
+        }
         if (lane == 0) {
-            float zk = 0.f;
-            for (int r = 0; r < p.k; ++r) zk += chosen_e[r];
-            const float den = p.renorm ? zk : z;
-            for (int r = 0; r < p.k; ++r) {
-                p.topk_id[tt * p.k + r] = chosen_i[r];
-                p.topk_w[tt * p.k + r] = chosen_e[r] / den;
-            }
-            float g = 1.0f;
-            if (p.shared_gate) g = 1.0f / (1.0f + __expf(-__ldcg(lg + p.E)));
-            p.gsh[tt] = g;
+            p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-__ldcg(lg + p.E))) : 1.0f;
             masks[tt][0] = m0;
             masks[tt][1] = m1;
         }
     }
     __syncthreads();
+    // expert union: thread e owns expert e; ballots give ascending slots
+    unsigned long long u0 = 0, u1 = 0;
+    for (int tt = 0; tt < p.T; ++tt) {
+        u0 |= masks[tt][0];
+        u1 |= masks[tt][1];
+    }
+    const int ue = threadIdx.x;
+    const bool in_union = ue < p.E && (ue < 64 ? ((u0 >> ue) & 1ull) : ((u1 >> (ue - 64)) & 1ull));
+    const bool local_on = in_union && ue >= p.e_lo && ue < p.e_hi;
+    const unsigned ball = __ballot_sync(0xffffffffu, local_on);
+    if (lane == 0 && warp < kMaxExperts / 32) s_warp_on[warp] = __popc(ball);
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp && w < kMaxExperts / 32; ++w) base += s_warp_on[w];
+    int n_local = 0;
+    for (int w = 0; w < kMaxExperts / 32; ++w) n_local += s_warp_on[w];
+    if (local_on) {
+        const int slot = base + __popc(ball & ((1u << lane) - 1u));
+        p.list[slot] = ue - p.e_lo;
+        for (int tt = 0; tt < kMaxT; ++tt) {
+            int rank = -1;
+            if (tt < p.T)
+                for (int r = 0; r < p.k; ++r)
+                    if (s_topk[tt * p.k + r] == ue) rank = r;
+            p.route_rank[slot * kMaxT + tt] = rank;
+        }
+    }
     if (threadIdx.x == 0) {
-        unsigned long long u0 = 0, u1 = 0;
-        for (int tt = 0; tt < p.T; ++tt) {
-            u0 |= masks[tt][0];
-            u1 |= masks[tt][1];
-        }
         *p.union_size = __popcll(u0) + __popcll(u1);
-        int n = 0;
-        for (int ei = p.e_lo; ei < p.e_hi; ++ei) {
-            const bool on = ei < 64 ? ((u0 >> ei) & 1ull) : ((u1 >> (ei - 64)) & 1ull);
-            if (!on) continue;
-            p.list[n] = ei - p.e_lo;
-            for (int tt = 0; tt < kMaxT; ++tt) {
-                int rank = -1;
-                if (tt < p.T)
-                    for (int r = 0; r < p.k; ++r)
-                        if (p.topk_id[tt * p.k + r] == ei) rank = r;
-                p.route_rank[n * kMaxT + tt] = rank;
-            }
-            ++n;
-        }
         const int n_local_routed = p.e_hi - p.e_lo;
-        int lb = 0;
-        for (int b = 0; b < p.S; ++b) {
-            if (b % p.ep_size != p.ep_rank) continue;
+        int n = n_local, lb = 0;
+        for (int b2 = 0; b2 < p.S; ++b2) {
+            if (b2 % p.ep_size != p.ep_rank) continue;
             p.list[n] = n_local_routed + lb;
-            for (int tt = 0; tt < kMaxT; ++tt) p.route_rank[n * kMaxT + tt] = tt < p.T ? p.k + b : -1;
+            for (int tt = 0; tt < kMaxT; ++tt) p.route_rank[n * kMaxT + tt] = tt < p.T ? p.k + b2 : -1;
             ++n;
             ++lb;
         }

@@ -48,11 +48,11 @@ def oracle_greedy(shape, prompt, n):
     om = OracleModel(shape, cb.TINY_SEED)
     os_ = OracleSession(om, 1024)
     os_.prefill(prompt)
-    bad = os_.min_router_margin() < 1e-2
+    bad = os_.min_router_margin() < 5e-2
     out, flagged = [], []
     for _ in range(n):
         acc, am, lg, mg, us = os_.verify([])
-        bad = bad or os_.min_router_margin() < 1e-2 or mg[0] < 5e-2
+        bad = bad or os_.min_router_margin() < 5e-2 or mg[0] < 5e-2
         out.append(int(am[0]))
         flagged.append(bad)
     return out, flagged

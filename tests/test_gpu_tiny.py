@@ -138,7 +138,7 @@ def greedy_sequence(om, p, n):
     return seq
 
 
-ROUTER_FLAG = 1e-2  # router decision gaps below this (logit units) are flagged near-ties
+ROUTER_FLAG = 5e-2  # router decision gaps below this (logit units) are flagged near-ties
 
 
 @pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
