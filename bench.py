@@ -265,12 +265,13 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = total_ms / args.steps
     value = float(np.mean([per_k_us[K] for K in KS]))
 
-    # ---- roofline: per-launch event timing of one eager step per K (same kernels, same stream)
+    # ---- roofline: in-graph per-kernel durations of one captured step per K
+    #      (globaltimer start stamps of consecutive kernels on the graph timeline)
     peak, peak_kind = measured_peaks()
     per_k = {}
     exp_bytes = exp_ns = 0.0
     for K in KS:
-        ns, kind = sess.profile(K)
+        ns, kind = sess.trace(K)
         us = sess.union_sizes()
         T = K + 1
         b = shape.step_bytes(us, ctx, T)

@@ -187,6 +187,13 @@ CASCADE_API void* cascade_session_stream(cascade_session* s);
  * all-reduce.  Returns the number of launches via *n (<= cap). */
 CASCADE_API int cascade_profile_step(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n);
 
+/* In-graph trace of one step of width K+1 (captured path, commit = 0):
+ * every kernel stamps %globaltimer when it starts (after its programmatic
+ * dependency wait), so ns[i] = start(i+1) - start(i) is kernel i's share
+ * of the step on the real graph timeline; kind[i] uses the classes of
+ * cascade_profile_step. */
+CASCADE_API int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n);
+
 /* Number of kernel launches one step of width K+1 performs (graph nodes
  * that are kernels). */
 CASCADE_API int cascade_step_kernel_count(cascade_session* s, int K, int* out);

@@ -580,6 +580,9 @@ struct orc_session {
     uint16_t* kc; /* [L][KV][max_ctx][hd] */
     uint16_t* vc;
     double min_router_margin; /* smallest router decision gap seen (flags near-ties) */
+    int last_T;               /* routing of the last forward: [L][T][k] ids, [L][T] margins */
+    int32_t* last_topk;
+    double* last_margin;
 };
 
 orc_session* orc_session_create(orc_model* m, int max_ctx) {
@@ -591,17 +594,29 @@ orc_session* orc_session_create(orc_model* m, int max_ctx) {
     s->kc = (uint16_t*)calloc(n, 2);
     s->vc = (uint16_t*)calloc(n, 2);
     s->min_router_margin = INFINITY;
+    s->last_topk = (int32_t*)calloc((size_t)m->L * 64 * m->k, sizeof(int32_t));
+    s->last_margin = (double*)calloc((size_t)m->L * 64, sizeof(double));
     return s;
 }
 
 void orc_session_destroy(orc_session* s) {
     if (!s) return;
+    free(s->last_topk);
+    free(s->last_margin);
     free(s->kc);
     free(s->vc);
     free(s);
 }
 
 int orc_cache_len(const orc_session* s) { return s ? s->len : -1; }
+
+int orc_last_routing(const orc_session* s, int32_t* topk, double* margin) {
+    if (!s) return -1;
+    const int n = s->m->L * s->last_T;
+    if (topk) memcpy(topk, s->last_topk, (size_t)n * s->m->k * sizeof(int32_t));
+    if (margin) memcpy(margin, s->last_margin, (size_t)n * sizeof(double));
+    return s->last_T;
+}
 
 double orc_min_router_margin(orc_session* s, int reset) {
     if (!s) return -1.0;
@@ -642,6 +657,11 @@ static int forward(orc_session* s, const int32_t* toks, int T, double* logits, i
         orc_router(m, l, xn, T, NULL, topk, topw, gsh, rmg);
         for (int t = 0; t < T; ++t)
             if (rmg[t] < s->min_router_margin) s->min_router_margin = rmg[t];
+        if (T <= 64) {
+            s->last_T = T;
+            memcpy(s->last_topk + (size_t)l * T * m->k, topk, (size_t)T * m->k * sizeof(int32_t));
+            memcpy(s->last_margin + (size_t)l * T, rmg, (size_t)T * sizeof(double));
+        }
         if (union_sizes) union_sizes[l] = orc_union(topk, T, m->k, NULL);
         orc_moe(m, l, xn, T, topk, topw, gsh, a);
         for (long i = 0; i < (long)T * d; ++i) x[i] += a[i];

@@ -79,6 +79,8 @@ int orc_cache_len(const orc_session* s);
 /* smallest router top-k decision margin (logit units) seen since the last
  * reset: a device/oracle routing disagreement below it is a flagged tie */
 double orc_min_router_margin(orc_session* s, int reset);
+/* routing of the last forward pass: topk [L][T][k], margins [L][T]; returns T */
+int orc_last_routing(const orc_session* s, int32_t* topk, double* margin);
 
 #ifdef __cplusplus
 }

@@ -51,6 +51,7 @@ def lib():
             "orc_verify": (c, [P, I32P, c, DP, I32P, DP, I32P]),
             "orc_cache_len": (c, [P]),
             "orc_min_router_margin": (ctypes.c_double, [P, c]),
+            "orc_last_routing": (c, [P, I32P, DP]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -203,6 +204,13 @@ class OracleSession:
         acc = _chk(lib().orc_verify(self.h, _p(d, ctypes.c_int32) if K else None, K, _p(logits, ctypes.c_double),
                                     _p(am, ctypes.c_int32), _p(mg, ctypes.c_double), _p(us, ctypes.c_int32)))
         return acc, am, logits, mg, us
+
+    def last_routing(self):
+        s = self.model.shape
+        tk = np.zeros((s.num_layers * 64, s.top_k), np.int32)
+        mg = np.zeros(s.num_layers * 64)
+        T = lib().orc_last_routing(self.h, _p(tk, ctypes.c_int32), _p(mg, ctypes.c_double))
+        return tk[: s.num_layers * T].reshape(s.num_layers, T, s.top_k), mg[: s.num_layers * T].reshape(s.num_layers, T)
 
     def min_router_margin(self, reset=True):
         return lib().orc_min_router_margin(self.h, 1 if reset else 0)

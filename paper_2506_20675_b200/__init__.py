@@ -225,6 +225,10 @@ def lib() -> ctypes.CDLL:
         "cascade_sync": (ctypes.c_int, [P]),
         "cascade_session_stream": (P, [P]),
         "cascade_step_kernel_count": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "cascade_step_trace": (
+            ctypes.c_int,
+            [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
+        ),
         "cascade_profile_step": (
             ctypes.c_int,
             [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
@@ -410,6 +414,16 @@ class Session:
         n = ctypes.c_int()
         _check(lib().cascade_profile_step(self.h, K, ns.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _i32p(kind),
                                           cap, ctypes.byref(n)))
+        return ns[: n.value], kind[: n.value]
+
+    def trace(self, K: int):
+        """In-graph per-kernel durations (ns) and classes of one captured step."""
+        cap = 64 * self.model.shape.num_layers + 16
+        ns = np.zeros(cap)
+        kind = np.zeros(cap, np.int32)
+        n = ctypes.c_int()
+        _check(lib().cascade_step_trace(self.h, K, ns.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _i32p(kind),
+                                        cap, ctypes.byref(n)))
         return ns[: n.value], kind[: n.value]
 
     def enable_taps(self, on: bool = True):

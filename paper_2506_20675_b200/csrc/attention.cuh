@@ -34,6 +34,9 @@ struct AttnParams {
     float* part;             // [KV][R][max_chunks][hd + 2]
     int T, H, KV, max_ctx, max_chunks;
     float scale;             // 1/sqrt(hd)
+    const void* pf;          // weights to prefetch into L2 (the O projection)
+    unsigned long long pf_bytes;
+    unsigned long long* trace;
 };
 
 // rotate_half RoPE on the pair (i, i + hd/2)
@@ -80,6 +83,8 @@ template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
     griddep_wait();
     griddep_launch();
+    trace_start(p.trace);
+    prefetch_l2(p.pf, p.pf_bytes);
     constexpr int LD = HD + 8;
     constexpr int HALF = HD / 2;
     constexpr int NKS = HD / 16;      // k-steps of QK^T
@@ -293,6 +298,7 @@ struct AttnCombineParams {
     uint16_t* out_bfrag;   // [H*hd] B-frag
     float* tap;            // optional fp32 [T][H*hd]
     int T, H, KV, hd, max_chunks;
+    unsigned long long* trace;
 };
 
 constexpr int kMaxChunksSmem = 1024;
@@ -300,6 +306,7 @@ constexpr int kMaxChunksSmem = 1024;
 __global__ void attn_combine_kernel(AttnCombineParams p) {
     griddep_wait();
     griddep_launch();
+    trace_start(p.trace);
     __shared__ float scale_c[kMaxChunksSmem];
     __shared__ float red[32];
     const int t = blockIdx.x, h = blockIdx.y;

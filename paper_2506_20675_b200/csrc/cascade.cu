@@ -386,12 +386,15 @@ struct AcceptParams {
     const int* union_size;
     cascade_verify_out* res;
     int T, L, S;
+    unsigned long long* trace;  // start slot; slot+1 receives the step end
 };
 
 __global__ void accept_kernel(AcceptParams p) {
     griddep_wait();
+    trace_start(p.trace);
     if (threadIdx.x != 0) return;
     const uint64_t t_end = globaltimer();
+    if (p.trace) p.trace[1] = t_end;
     cascade_verify_out r;
     memset(&r, 0, sizeof(r));
     int am[kMaxT];
@@ -500,6 +503,10 @@ struct cascade_session {
     unsigned long long* stamps = nullptr;
     int* tokens_used = nullptr;
     float2* rope = nullptr;
+    unsigned long long* trace = nullptr;  // per-kernel start stamps of the last step
+    int trace_kind[kMaxT + 1][2048] = {};
+    int trace_n[kMaxT + 1] = {};
+    bool prefetch = true;
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -593,6 +600,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
         (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
+        (rc = salloc(s, &s->trace, 2048 * 8)) ||
         (rc = salloc(s, &s->kc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)) ||
         (rc = salloc(s, &s->vc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)))
         return fail(rc);
@@ -604,6 +612,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     }
     std::memset(s->h_params, 0, sizeof(StepParams));
     std::memset(s->h_result, 0, sizeof(cascade_verify_out));
+    if (const char* v = getenv("CASCADE_NO_PREFETCH")) s->prefetch = v[0] == '0';
     // attention smem opt-in
     const int asmem = D.hd == 32 ? attn_smem_bytes<32>() : D.hd == 64 ? attn_smem_bytes<64>() : attn_smem_bytes<128>();
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
@@ -707,6 +716,12 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     const cudaStream_t st = s->stream;
     const bool taps = s->taps_on;
     int nk = 0;
+    int slot = 0;
+    auto tr = [&](int kind) {
+        s->trace_kind[T][slot] = kind;
+        return s->trace + slot++;
+    };
+    const bool pf = s->prefetch;
     CK(cudaMemcpyAsync(s->d_params, s->h_params, sizeof(StepParams), cudaMemcpyHostToDevice, st));
 
     EmbedParams ep{};
@@ -726,6 +741,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ep.hd = D.hd;
     ep.rope_theta = (double)m->g.rope_theta;
     ep.eps = m->g.norm_eps;
+    ep.pf = pf ? m->layers[0].wqkv : nullptr;
+    ep.pf_bytes = pf ? D.wqkv_vec * 16 : 0;
+    ep.trace = tr(0);
     PB(0);
     CK(launch_k(embed_norm_kernel, dim3(T), dim3(kRouteThreads), 0, st, false, ep));
     PE();
@@ -744,6 +762,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         q.out = s->qkv;
         q.ld = D.qkvd;
         q.stamp = s->stamps + 1 + 2 * l;
+        q.trace = tr(1);
         PB(1);
         CK(launch_gemv(EPI_STORE, q, s->gemv_grid, st));
         PE();
@@ -762,6 +781,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ap.max_ctx = s->max_ctx;
         ap.max_chunks = s->max_chunks;
         ap.scale = 1.0f / sqrtf((float)D.hd);
+        ap.pf = pf ? w.wo : nullptr;
+        ap.pf_bytes = pf ? D.wo_vec * 16 : 0;
+        ap.trace = tr(2);
         const int agrid = m->num_sms;
         PB(2);
         if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, attn_smem_bytes<32>(), st, true, ap));
@@ -779,6 +801,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         cp.KV = D.KV;
         cp.hd = D.hd;
         cp.max_chunks = s->max_chunks;
+        cp.trace = tr(3);
         PB(3);
         CK(launch_k(attn_combine_kernel, dim3(T, D.H), dim3(D.hd), 0, st, true, cp));
         PE();
@@ -792,6 +815,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         o.n_ks = D.hq / 16;
         o.out = s->x;
         o.ld = D.d;
+        o.trace = tr(4);
         PB(4);
         CK(launch_gemv(EPI_ADD, o, s->gemv_grid, st));
         PE();
@@ -828,6 +852,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.eps = m->g.norm_eps;
         rp.zero_nonlocal = m->ep_size > 1;
         rp.stamp = s->stamps + 2 + 2 * l;
+        rp.trace = tr(5);
         PB(5);
         const int rgroups = (D.E + (m->g.shared_gate ? 1 : 0) + kRouteWarps - 1) / kRouteWarps;
         CK(launch_k(moe_route_kernel, dim3(T, rgroups), dim3(kRouteThreads), (size_t)D.d * 4, st, true, rp));
@@ -853,6 +878,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         gu.n_ks = D.d / 16;
         gu.hout = s->hbuf;
         gu.h_block_stride = (long long)D.f * 16;
+        gu.trace = tr(6);
         PB(6);
         CK(launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st));
         PE();
@@ -870,6 +896,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         dn.n_contrib = D.k + D.S;
         dn.out = s->ycontrib;
         dn.ld = D.d;
+        dn.trace = tr(7);
         PB(7);
         CK(launch_gemv(EPI_DOWN, dn, s->gemv_grid, st));
         PE();
@@ -896,6 +923,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.k = D.k;
         c.S = D.S;
         c.eps = m->g.norm_eps;
+        c.pf = (pf && l + 1 < D.L) ? m->layers[l + 1].wqkv : nullptr;
+        c.pf_bytes = (pf && l + 1 < D.L) ? D.wqkv_vec * 16 : 0;
+        c.trace = tr(8);
         PB(8);
         CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRouteThreads), 0, st, m->ep_size == 1, c));
         PE();
@@ -911,6 +941,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     lm.out = taps ? s->taps.final_logits : nullptr;
     lm.ld = D.V;
     lm.stamp = s->stamps + 1 + 2 * D.L;
+    lm.trace = tr(9);
     PB(9);
     CK(launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st));
     PE();
@@ -926,6 +957,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ap.T = T;
     ap.L = D.L;
     ap.S = D.S;
+    ap.trace = tr(10);
+    s->trace_n[T] = slot;
     PB(10);
     CK(launch_k(accept_kernel, dim3(1), dim3(32), 0, st, true, ap));
     PE();
@@ -984,6 +1017,31 @@ extern "C" int cascade_profile_step(cascade_session* s, int K, double* ns, int32
         CK(cudaEventElapsedTime(&ms, prof.ev[2 * i], prof.ev[2 * i + 1]));
         ns[i] = (double)ms * 1.0e6;
         kind[i] = prof.kind[i];
+    }
+    *n = cnt;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n) {
+    if (!s || !ns || !kind || !n || K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "bad arguments");
+    if (s->taps_on) return set_err(CASCADE_EINVAL, "step trace needs the captured path (disable taps)");
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    const int T = K + 1;
+    s->h_params->mode = 0;
+    s->h_params->commit = 0;
+    s->h_params->T = T;
+    s->h_params->t_base_ns = s->t_base_ns;
+    int rc = run_step(s, T);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(s->stream));
+    const int cnt = s->trace_n[T];
+    if (cnt > cap) return set_err(CASCADE_EINVAL, "trace buffer too small: need " + std::to_string(cnt));
+    std::vector<unsigned long long> st(cnt + 1);
+    CK(cudaMemcpy(st.data(), s->trace, (cnt + 1) * 8, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < cnt; ++i) {
+        ns[i] = (double)st[i + 1] - (double)st[i];
+        kind[i] = s->trace_kind[T][i];
     }
     *n = cnt;
     return CASCADE_OK;

@@ -29,12 +29,44 @@ constexpr int kTPW = 4;                 // 16-row tiles per super-tile (per warp
 constexpr int kSTRows = 16 * kTPW;      // 64 rows per super-tile
 constexpr int kMaxT = 16;               // tokens in flight (two n8 tiles)
 
+__device__ __forceinline__ uint64_t globaltimer_raw() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Programmatic dependent launch: every kernel of the step waits for its
 // predecessor's completion (and memory) before touching any data, so the
 // chain stays transitively ordered while launch latency and CTA
 // rasterisation overlap the predecessor's tail.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Bulk L2 prefetch of an upcoming weight matrix, spread over every thread
+// of the grid.  Issued from latency-bound kernels (attention, combine) so
+// HBM keeps streaming the next dense GEMV's weights into the 126 MB L2
+// while those kernels wait on latency.
+__device__ __forceinline__ void prefetch_l2(const void* base, unsigned long long bytes) {
+    if (base == nullptr || bytes == 0) return;
+    constexpr unsigned long long kChunkB = 16384;
+    const unsigned long long n = (bytes + kChunkB - 1) / kChunkB;
+    const unsigned long long nthr = (unsigned long long)gridDim.x * gridDim.y * blockDim.x;
+    const unsigned long long me =
+        ((unsigned long long)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    for (unsigned long long c = me; c < n; c += nthr) {
+        const unsigned long long off = c * kChunkB;
+        unsigned long long sz = bytes - off < kChunkB ? bytes - off : kChunkB;
+        sz &= ~15ull;
+        if (sz == 0) continue;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)base + off), "r"((uint32_t)sz)
+                     : "memory");
+    }
+}
+
+// per-kernel start stamp for in-graph tracing (block 0, thread 0)
+__device__ __forceinline__ void trace_start(unsigned long long* slot) {
+    if (slot != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *slot = globaltimer_raw();
+}
 
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;

@@ -57,6 +57,7 @@ struct GemvParams {
     int n_contrib;             // EPI_DOWN
     unsigned long long* keys;  // EPI_ARGMAX
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
+    unsigned long long* trace; // in-graph trace slot
 };
 
 constexpr int kGemvThreads = 256;
@@ -215,6 +216,7 @@ constexpr int gemv_smem_bytes() {
 template <int NT, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams p) {
     griddep_wait();
+    trace_start(p.trace);
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
     extern __shared__ float4 red[];  // [warp][slot][kTPW*NT*32]
     __shared__ long long seg_unit[kGemvWarps][2];

@@ -65,11 +65,13 @@ struct RouteParams {
     float eps;
     int zero_nonlocal;
     unsigned long long* stamp;   // MoE-block start (CostBreakdown split)
+    unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p) {
     griddep_wait();
     griddep_launch();
+    trace_start(p.trace);
     __shared__ float red[32];
     __shared__ int s_last;
     __shared__ unsigned long long masks[kMaxT][2];
@@ -253,11 +255,16 @@ struct CombineParams {
     float* tap_x;                // optional [T][d] residual after the add
     int T, d, k, S;
     float eps;
+    const void* pf;              // next layer's QKV weights -> L2
+    unsigned long long pf_bytes;
+    unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(kRouteThreads) moe_combine_kernel(CombineParams p) {
     griddep_wait();
     griddep_launch();
+    trace_start(p.trace);
+    prefetch_l2(p.pf, p.pf_bytes);
     __shared__ float red[32];
     __shared__ float wsh[kMaxTopK + 1];
     const int t = blockIdx.x;
@@ -353,11 +360,16 @@ struct EmbedParams {
     int T, d, hd;
     double rope_theta;
     float eps;
+    const void* pf;              // layer-0 QKV weights -> L2
+    unsigned long long pf_bytes;
+    unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p) {
     griddep_wait();
     griddep_launch();
+    trace_start(p.trace);
+    prefetch_l2(p.pf, p.pf_bytes);
     __shared__ float red[32];
     const int t = blockIdx.x;
     if (t == 0 && threadIdx.x == 0) *p.stamp = globaltimer();

@@ -44,15 +44,15 @@ def repetitive_prompt(n=64, seed=1):
 
 def oracle_greedy(shape, prompt, n):
     """Oracle K=0 decode; flagged[i] marks a near-tie at or before token i
-    (router gap < 1e-2 anywhere, prefill included, or LM top-2 gap < 5e-2)."""
+    (router gap < 2e-3 anywhere, prefill included, or LM top-2 gap < 5e-2)."""
     om = OracleModel(shape, cb.TINY_SEED)
     os_ = OracleSession(om, 1024)
     os_.prefill(prompt)
-    bad = os_.min_router_margin() < 5e-2
+    bad = os_.min_router_margin() < 2e-3
     out, flagged = [], []
     for _ in range(n):
         acc, am, lg, mg, us = os_.verify([])
-        bad = bad or os_.min_router_margin() < 5e-2 or mg[0] < 5e-2
+        bad = bad or os_.min_router_margin() < 2e-3 or mg[0] < 5e-2
         out.append(int(am[0]))
         flagged.append(bad)
     return out, flagged

@@ -138,7 +138,8 @@ def greedy_sequence(om, p, n):
     return seq
 
 
-ROUTER_FLAG = 5e-2  # router decision gaps below this (logit units) are flagged near-ties
+PREFILL_ROUTER_FLAG = 2e-3  # prefill routing is not tapped: flag oracle gaps below this
+ROUTER_FLIP_BOUND = 2e-2   # a device/oracle routing disagreement needs an oracle gap below this
 
 
 @pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
@@ -146,24 +147,24 @@ def test_end_to_end_greedy_decode(tiny, K):
     """Lock-step decode, device vs independent oracle (no teacher forcing):
     drafts are the true greedy continuation with random corruptions, so
     every accepted count 0..K occurs.  Logits must agree within the stated
-    tolerance; argmax rows, accepted counts, KV length and per-layer union
-    sizes must agree exactly.  A comparison stops at the first flagged
-    near-tie (an oracle router decision gap < ROUTER_FLAG anywhere, prefill
-    included, or an LM top-2 gap inside the observed logit error), after
-    which the two decodes may legitimately diverge; several prompts are
-    tried so that enough clean lock-step verifies are compared."""
+    tolerance; argmax rows, accepted counts, KV length, per-layer routing
+    and union sizes must agree exactly.  Near-ties are handled explicitly:
+    a routing disagreement is legal only where the oracle's decision gap is
+    below ROUTER_FLIP_BOUND (then the decodes legitimately diverge and the
+    comparison of that prompt stops), likewise an argmax disagreement only
+    inside the observed logit error."""
     shape, m, om = tiny
     clean_steps = 0
     worst = 0.0
-    for trial in range(8):
+    for trial in range(6):
         p = prompt(24, seed=100 * K + trial)
         truth = greedy_sequence(om, p, 60)
         s = cb.Session(m, max_ctx=512, k_max=8)
-        s.enable_taps(True)  # eager path + final logits tap
+        s.enable_taps(True)  # eager path + routing / logits taps
         s.prefill(p)
         os_ = OracleSession(om, 512)
         os_.prefill(p)
-        if os_.min_router_margin() < ROUTER_FLAG:
+        if os_.min_router_margin() < PREFILL_ROUTER_FLAG:
             s.close()
             continue
         rng = np.random.default_rng(K + trial)
@@ -175,16 +176,20 @@ def test_end_to_end_greedy_decode(tiny, K):
                     drafts[i] = rng.integers(0, shape.vocab)
             g = s.verify(drafts)
             acc, am, lg, mg, us = os_.verify(drafts)
-            if os_.min_router_margin() < ROUTER_FLAG:
-                break
             T = K + 1
+            otk, omg = os_.last_routing()
+            gtk = s.tap("topk_id")[:, :T]
+            if not np.array_equal(gtk, otk):
+                bad = np.any(gtk != otk, axis=2)
+                assert np.all(omg[bad] < ROUTER_FLIP_BOUND), (trial, pos, omg[bad])
+                break  # flagged near-tie flip
             glog = s.tap("final_logits")[:T]
             err = float(np.abs(glog - lg).max())
             worst = max(worst, err)
             assert err <= LOGIT_ATOL + LOGIT_RTOL * np.abs(lg).max(), (trial, pos, err)
-            if np.any(mg[:T] <= 2 * err + MARGIN):
-                break
-            assert list(g.argmax[:T]) == list(am), (trial, pos)
+            if list(g.argmax[:T]) != list(am):
+                assert np.all(mg[np.array(g.argmax[:T]) != am] <= 2 * err + MARGIN), (trial, pos)
+                break  # flagged LM near-tie
             assert g.accepted == acc
             assert g.emitted == acc + 1
             assert g.cache_len == os_.cache_len
