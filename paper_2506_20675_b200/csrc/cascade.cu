@@ -612,7 +612,10 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     }
     std::memset(s->h_params, 0, sizeof(StepParams));
     std::memset(s->h_result, 0, sizeof(cascade_verify_out));
-    if (const char* v = getenv("CASCADE_NO_PREFETCH")) s->prefetch = v[0] == '0';
+    // Bulk L2 prefetch from latency-bound kernels measured slower on B200
+    // (the issuing kernels stall on the bulk-prefetch queue); off by default.
+    s->prefetch = false;
+    if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
     // attention smem opt-in
     const int asmem = D.hd == 32 ? attn_smem_bytes<32>() : D.hd == 64 ? attn_smem_bytes<64>() : attn_smem_bytes<128>();
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);

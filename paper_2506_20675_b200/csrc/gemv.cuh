@@ -62,7 +62,7 @@ struct GemvParams {
 
 constexpr int kGemvThreads = 256;
 constexpr int kGemvWarps = kGemvThreads / 32;
-constexpr int kUnroll = 4;
+
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
@@ -215,15 +215,50 @@ constexpr int gemv_smem_bytes() {
 // function of (U, grid), so results are deterministic.
 template <int NT, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams p) {
+    extern __shared__ float4 red[];  // [warp][slot][kTPW*NT*32]
+    __shared__ long long seg_unit[kGemvWarps][2];
+    constexpr int kSlot = kTPW * NT * 32;
+    constexpr int kUnroll = NT == 1 ? 4 : 3;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint64_t pol = policy_evict_first();
+
+    // PDL prologue: a dense job's weights do not depend on the previous
+    // kernel, so the first kUnroll k-steps of every warp are requested
+    // *before* griddepcontrol.wait and stream in while the predecessor
+    // (attention combine / expert combine) is still finishing.
+    uint4 a[kUnroll][kTPW];
+    bool pre = false;
+    if (p.list == nullptr && p.count == nullptr) {
+        const long long total0 = (long long)p.n_blocks * p.n_st * p.n_ks;
+        long long ncm = total0 / ((long long)p.min_seg * kGemvWarps);
+        if (ncm < 1) ncm = 1;
+        const int NC0 = (long long)gridDim.x < ncm ? (int)gridDim.x : (int)ncm;
+        if ((int)blockIdx.x < NC0) {
+            const long long clo0 = total0 * blockIdx.x / NC0, chi0 = total0 * (blockIdx.x + 1) / NC0;
+            const long long wlo0 = clo0 + (chi0 - clo0) * warp / kGemvWarps;
+            const long long whi0 = clo0 + (chi0 - clo0) * (warp + 1) / kGemvWarps;
+            const long long unit0 = wlo0 / p.n_ks;
+            const int ks00 = (int)(wlo0 - unit0 * p.n_ks);
+            const long long rem0 = whi0 - wlo0;
+            const int ks10 = rem0 < (long long)(p.n_ks - ks00) ? ks00 + (int)rem0 : p.n_ks;
+            if (ks10 - ks00 >= kUnroll) {
+                const int bl0 = (int)(unit0 / p.n_st);
+                const int st0 = (int)(unit0 - (long long)bl0 * p.n_st);
+                const uint4* A0 = p.W + (long long)bl0 * p.w_block_stride +
+                                  (long long)st0 * p.n_ks * (kTPW * 32) + lane;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int it = 0; it < kTPW; ++it)
+                        a[u][it] = ldg_stream(A0 + ((long long)(ks00 + u) * kTPW + it) * 32, pol);
+                pre = true;
+            }
+        }
+    }
     griddep_wait();
     trace_start(p.trace);
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
-    extern __shared__ float4 red[];  // [warp][slot][kTPW*NT*32]
-    __shared__ long long seg_unit[kGemvWarps][2];
-    __shared__ int s_last;
-    constexpr int kSlot = kTPW * NT * 32;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
     const int U = p.count ? *p.count : p.n_blocks;
     const long long per_block = (long long)p.n_st * p.n_ks;
     const long long total = (long long)U * per_block;
@@ -241,7 +276,6 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         seg_unit[warp][1] = -1;
     }
     __syncwarp();
-    const uint64_t pol = policy_evict_first();
 
     float acc[kTPW][NT][4];
     long long pos = wlo;
@@ -258,13 +292,15 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         zero_acc<NT>(acc);
         int s = ks0;
         for (; s + kUnroll <= ks1; s += kUnroll) {
-            uint4 a[kUnroll][kTPW];
             uint2 b[kUnroll][NT];
+            if (!pre) {
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+                for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-                for (int it = 0; it < kTPW; ++it)
-                    a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+                    for (int it = 0; it < kTPW; ++it)
+                        a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+            }
+            pre = false;
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
@@ -277,16 +313,16 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
                     for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], b[u][nt]);
         }
         for (; s < ks1; ++s) {
-            uint4 a[kTPW];
+            uint4 a1[kTPW];
             uint2 b[NT];
 #pragma unroll
-            for (int it = 0; it < kTPW; ++it) a[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
+            for (int it = 0; it < kTPW; ++it) a1[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) b[nt] = ldg_act(Bp + (s * 2 + nt) * 32);
 #pragma unroll
             for (int it = 0; it < kTPW; ++it)
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[it], b[nt]);
+                for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], b[nt]);
         }
         const bool first_seg = pos == wlo;
         pos += ks1 - ks0;
@@ -336,7 +372,6 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         if (lane == 0) p.counters[unit] = 0;
         gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
     }
-    (void)s_last;
 }
 
 }  // namespace cascade
