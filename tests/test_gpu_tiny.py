@@ -138,13 +138,34 @@ def greedy_sequence(om, p, n):
     return seq
 
 
-PREFILL_ROUTER_FLAG = 2e-3  # prefill routing is not tapped: flag oracle gaps below this
 # End to end (no teacher forcing) the random-init tiny model amplifies the
 # bf16 rounding-flip noise of each stage (~1e-4, see the teacher-forced
 # test) to ~1.5% of the logit range after 4 layers; the bounds below state
 # that.  Teacher-forced stage bars are 100x tighter.
 E2E_LOGIT_RTOL = 3e-2
 ROUTER_FLIP_BOUND = 0.25   # a device/oracle routing disagreement needs an oracle gap below this
+
+
+def lockstep_prefill(s, os_, p):
+    """Prefill device and oracle in the same <=16-token chunks (both sides
+    chunk at 16; consecutive chunks overlap by the pending token) and compare
+    every chunk's per-layer routing.  A disagreement is legal only where the
+    oracle's own decision gap is below ROUTER_FLIP_BOUND; it is flagged and
+    the prompt is skipped (its decodes legitimately diverge)."""
+    pos = 0
+    while pos < len(p) - 1:
+        end = min(pos + 17, len(p))
+        s.prefill(p[pos:end])
+        os_.prefill(p[pos:end])
+        otk, omg = os_.last_routing()
+        T = otk.shape[1]
+        gtk = s.tap("topk_id")[:, :T]
+        if not np.array_equal(gtk, otk):
+            bad = np.any(gtk != otk, axis=2)
+            assert np.all(omg[bad] < ROUTER_FLIP_BOUND), omg[bad]
+            return False
+        pos = end - 1
+    return True
 
 
 @pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
@@ -161,17 +182,15 @@ def test_end_to_end_greedy_decode(tiny, K):
     shape, m, om = tiny
     clean_steps = 0
     worst = 0.0
-    for trial in range(6):
+    for trial in range(8):
         p = prompt(24, seed=100 * K + trial)
         truth = greedy_sequence(om, p, 60)
         s = cb.Session(m, max_ctx=512, k_max=8)
         s.enable_taps(True)  # eager path + routing / logits taps
-        s.prefill(p)
         os_ = OracleSession(om, 512)
-        os_.prefill(p)
-        if os_.min_router_margin() < PREFILL_ROUTER_FLAG:
+        if not lockstep_prefill(s, os_, p):
             s.close()
-            continue
+            continue  # flagged near-tie flip inside the prompt
         rng = np.random.default_rng(K + trial)
         pos = 0
         while pos + K < len(truth):
