@@ -507,6 +507,9 @@ struct cascade_session {
     int trace_kind[kMaxT + 1][2048] = {};
     int trace_n[kMaxT + 1] = {};
     bool prefetch = true;
+    int l2_prologue = 0;  // measured slower (down-proj ranges exceed L2; QKV prefetch slows the combine)
+    int gemv_trigger = 0;  // early launch_dependents from the GEMVs measured slower (A/B in profiles/r01)
+    int down_early = 1;
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -616,6 +619,9 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     // (the issuing kernels stall on the bulk-prefetch queue); off by default.
     s->prefetch = false;
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
+    if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = v[0] == '1';
+    if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
+    if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     // attention smem opt-in
     const int asmem = D.hd == 32 ? attn_smem_bytes<32>() : D.hd == 64 ? attn_smem_bytes<64>() : attn_smem_bytes<128>();
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
@@ -684,6 +690,8 @@ static GemvParams gemv_base(cascade_session* s, int T) {
     p.partial = s->partial;
     p.counters = s->counters;
     p.n_blocks = 1;
+    p.l2_prologue = s->l2_prologue;
+    p.trigger = s->gemv_trigger;
     return p;
 }
 
@@ -896,6 +904,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         dn.n_st = D.d / kSTRows;
         dn.n_ks = D.f / 16;
         dn.route_rank = s->route_rank;
+        dn.early_list = s->down_early && s->gemv_trigger;  // list/count from moe_route, two kernels back
         dn.n_contrib = D.k + D.S;
         dn.out = s->ycontrib;
         dn.ld = D.d;

@@ -58,6 +58,9 @@ struct GemvParams {
     unsigned long long* keys;  // EPI_ARGMAX
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
     unsigned long long* trace; // in-graph trace slot
+    int early_list;            // list/count final before griddepcontrol.wait (expert down projection)
+    int l2_prologue;           // also L2-prefetch the rest of each warp's range before the wait
+    int trigger;               // griddepcontrol.launch_dependents right after the wait
 };
 
 constexpr int kGemvThreads = 256;
@@ -229,12 +232,18 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     // (attention combine / expert combine) is still finishing.
     uint4 a[kUnroll][kTPW];
     bool pre = false;
-    if (p.list == nullptr && p.count == nullptr) {
-        const long long total0 = (long long)p.n_blocks * p.n_st * p.n_ks;
+    const bool dense = p.list == nullptr && p.count == nullptr;
+    if (dense || p.early_list) {
+        // weights addressable now: dense matrices always; the expert down
+        // projection because its active list was written two kernels back
+        // and the gate/up kernel triggers its dependents only after its own
+        // griddepcontrol.wait.
+        const int U0 = dense ? p.n_blocks : __ldcg(p.count);
+        const long long total0 = (long long)U0 * p.n_st * p.n_ks;
         long long ncm = total0 / ((long long)p.min_seg * kGemvWarps);
         if (ncm < 1) ncm = 1;
         const int NC0 = (long long)gridDim.x < ncm ? (int)gridDim.x : (int)ncm;
-        if ((int)blockIdx.x < NC0) {
+        if ((int)blockIdx.x < NC0 && total0 > 0) {
             const long long clo0 = total0 * blockIdx.x / NC0, chi0 = total0 * (blockIdx.x + 1) / NC0;
             const long long wlo0 = clo0 + (chi0 - clo0) * warp / kGemvWarps;
             const long long whi0 = clo0 + (chi0 - clo0) * (warp + 1) / kGemvWarps;
@@ -242,10 +251,12 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
             const int ks00 = (int)(wlo0 - unit0 * p.n_ks);
             const long long rem0 = whi0 - wlo0;
             const int ks10 = rem0 < (long long)(p.n_ks - ks00) ? ks00 + (int)rem0 : p.n_ks;
+            long long pf_from = wlo0;
             if (ks10 - ks00 >= kUnroll) {
                 const int bl0 = (int)(unit0 / p.n_st);
                 const int st0 = (int)(unit0 - (long long)bl0 * p.n_st);
-                const uint4* A0 = p.W + (long long)bl0 * p.w_block_stride +
+                const int blk0 = p.list ? __ldcg(p.list + bl0) : bl0;
+                const uint4* A0 = p.W + (long long)blk0 * p.w_block_stride +
                                   (long long)st0 * p.n_ks * (kTPW * 32) + lane;
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u)
@@ -253,10 +264,33 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
                     for (int it = 0; it < kTPW; ++it)
                         a[u][it] = ldg_stream(A0 + ((long long)(ks00 + u) * kTPW + it) * 32, pol);
                 pre = true;
+                pf_from = wlo0 + kUnroll;
+            }
+            if (p.l2_prologue && lane == 0) {
+                // the rest of this warp's range -> L2 while the predecessor drains
+                for (long long pos = pf_from; pos < whi0;) {
+                    const long long unit = pos / p.n_ks;
+                    const int ks = (int)(pos - unit * p.n_ks);
+                    long long n = p.n_ks - ks;
+                    if (whi0 - pos < n) n = whi0 - pos;
+                    const int bl = (int)(unit / p.n_st);
+                    const int st = (int)(unit - (long long)bl * p.n_st);
+                    const int blk = p.list ? __ldcg(p.list + bl) : bl;
+                    const char* src = reinterpret_cast<const char*>(
+                        p.W + (long long)blk * p.w_block_stride + ((long long)st * p.n_ks + ks) * (kTPW * 32));
+                    const unsigned long long bytes = (unsigned long long)n * kTPW * 32 * 16;
+                    for (unsigned long long off = 0; off < bytes; off += 65536) {
+                        const unsigned long long sz = bytes - off < 65536 ? bytes - off : 65536;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"((uint32_t)sz)
+                                     : "memory");
+                    }
+                    pos += n;
+                }
             }
         }
     }
     griddep_wait();
+    if (p.trigger) griddep_launch();
     trace_start(p.trace);
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
     const int U = p.count ? *p.count : p.n_blocks;

@@ -146,6 +146,16 @@ E2E_LOGIT_RTOL = 3e-2
 ROUTER_FLIP_BOUND = 0.25   # a device/oracle routing disagreement needs an oracle gap below this
 
 
+def assert_first_flip_is_near_tie(gtk, otk, omg):
+    """Routing disagreement [L, T, k]: only the first layer that disagrees
+    is an independent event (a flipped token's MoE output, hence its next-
+    layer routing and every later KV row, legitimately differs after it);
+    every disagreeing row there must be an oracle near-tie."""
+    bad = np.any(gtk != otk, axis=2)
+    l0 = int(np.argmax(bad.any(axis=1)))
+    assert np.all(omg[l0][bad[l0]] < ROUTER_FLIP_BOUND), (l0, omg[l0][bad[l0]])
+
+
 def lockstep_prefill(s, os_, p):
     """Prefill device and oracle in the same <=16-token chunks (both sides
     chunk at 16; consecutive chunks overlap by the pending token) and compare
@@ -161,8 +171,7 @@ def lockstep_prefill(s, os_, p):
         T = otk.shape[1]
         gtk = s.tap("topk_id")[:, :T]
         if not np.array_equal(gtk, otk):
-            bad = np.any(gtk != otk, axis=2)
-            assert np.all(omg[bad] < ROUTER_FLIP_BOUND), omg[bad]
+            assert_first_flip_is_near_tie(gtk, otk, omg)
             return False
         pos = end - 1
     return True
@@ -204,8 +213,7 @@ def test_end_to_end_greedy_decode(tiny, K):
             otk, omg = os_.last_routing()
             gtk = s.tap("topk_id")[:, :T]
             if not np.array_equal(gtk, otk):
-                bad = np.any(gtk != otk, axis=2)
-                assert np.all(omg[bad] < ROUTER_FLIP_BOUND), (trial, pos, omg[bad])
+                assert_first_flip_is_near_tie(gtk, otk, omg)
                 break  # flagged near-tie flip
             glog = s.tap("final_logits")[:T]
             err = float(np.abs(glog - lg).max())
