@@ -72,7 +72,7 @@ typedef struct cascade_geometry {
     int32_t top_k;              /* routed experts per token */
     int32_t shared_experts;     /* always-active expert blocks of width d_ff */
     /* --- tensor shape (public model configs; not in the reference) --- */
-    int32_t d_model;            /* hidden size d (multiple of 64) */
+    int32_t d_model;            /* hidden size d (multiple of 256) */
     int32_t d_ff;               /* routed expert intermediate f (multiple of 32) */
     int32_t n_heads;            /* query heads H */
     int32_t n_kv_heads;         /* key/value heads (GQA) */

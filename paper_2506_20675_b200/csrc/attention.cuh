@@ -18,6 +18,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "gemv_umma.cuh"
 
 namespace cascade {
 
@@ -79,12 +80,16 @@ constexpr int attn_smem_bytes() {
 //
 // smem (bf16, row stride HD+8 -> conflict-free fragment loads):
 //   q_hi [kAttnMaxRows][HD+8] | q_lo [..] | k [kChunk][HD+8] | v [kChunk][HD+8]
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
-    griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
-    prefetch_l2(p.pf, p.pf_bytes);
     constexpr int LD = HD + 8;
     constexpr int HALF = HD / 2;
     constexpr int NKS = HD / 16;      // k-steps of QK^T
@@ -97,7 +102,35 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
 
     const int G = p.H / p.KV;
     const int R = G * p.T;
+    // The committed cache (and its length, written by the previous step's
+    // accept kernel) does not depend on the predecessor (the QKV GEMV): the
+    // first item's K/V chunk is requested with cp.async before the wait.
     const int ctx = *p.ctx_ptr;
+    auto issue_kv = [&](int item) {
+        const int c = item / p.KV;
+        const int kvh = item - c * p.KV;
+        const int key0 = c * kChunk;
+        const int nkeys = min(kChunk, ctx - key0);
+        constexpr int V8 = HD / 8;  // 16-byte pieces per row
+        const long long base = ((long long)kvh * p.max_ctx + key0) * HD;
+        for (int e = threadIdx.x; e < kChunk * V8; e += blockDim.x) {
+            const int j = e / V8, q = e - j * V8;
+            const bool ok = j < nkeys;
+            cp_async16(ks + j * LD + q * 8, p.kc + (ok ? base + (long long)e * 8 : 0), ok ? 16 : 0);
+            cp_async16(vs + j * LD + q * 8, p.vc + (ok ? base + (long long)e * 8 : 0), ok ? 16 : 0);
+        }
+        cp_async_commit();
+    };
+    const int nch0 = (ctx + kChunk - 1) / kChunk;
+    bool kv_pending = false;
+    if ((int)blockIdx.x < nch0 * p.KV) {
+        issue_kv(blockIdx.x);
+        kv_pending = true;
+    }
+    griddep_wait();
+    griddep_launch();
+    trace_start(p.trace);
+    prefetch_l2(p.pf, p.pf_bytes);
     const int nch = (ctx + kChunk - 1) / kChunk;
     const int n_items = (nch + 1) * p.KV;
     const int QD = (p.H + 2 * p.KV) * HD;
@@ -156,22 +189,11 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 vs[j * LD + i] = va;
                 vs[j * LD + i + HALF] = vb;
             }
-        } else {
-            constexpr int V8 = HD / 8;  // uint4 per row
-            const long long base = ((long long)kvh * p.max_ctx + key0) * HD;
-            const uint4* k8 = reinterpret_cast<const uint4*>(p.kc + base);
-            const uint4* v8 = reinterpret_cast<const uint4*>(p.vc + base);
-            for (int e = threadIdx.x; e < kChunk * V8; e += blockDim.x) {
-                const int j = e / V8, q = e - j * V8;
-                uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-                if (j < nkeys) {
-                    kk = __ldg(k8 + e);
-                    vv = __ldg(v8 + e);
-                }
-                *reinterpret_cast<uint4*>(ks + j * LD + q * 8) = kk;
-                *reinterpret_cast<uint4*>(vs + j * LD + q * 8) = vv;
-            }
+        } else if (!kv_pending) {
+            issue_kv(item);  // later items: the copy overlaps the query staging above
         }
+        kv_pending = false;
+        cp_async_wait_all();
         __syncthreads();
 
         for (int mt = warp; mt < n_mt; mt += kAttnThreads / 32) {
@@ -299,6 +321,7 @@ struct AttnCombineParams {
     float* tap;            // optional fp32 [T][H*hd]
     int T, H, KV, hd, max_chunks;
     unsigned long long* trace;
+    int umma;              // out_bfrag in the UMMA B layout (O projection on tcgen05)
 };
 
 constexpr int kMaxChunksSmem = 1024;
@@ -318,9 +341,20 @@ __global__ void attn_combine_kernel(AttnCombineParams p) {
     const int nch = (ctx + kChunk - 1) / kChunk + 1;
     const int stride = p.hd + 2;
     const float* base = p.part + ((long long)kvh * R + r) * p.max_chunks * stride;
-    float m = -INFINITY;
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) m = fmaxf(m, base[(long long)c * stride]);
-    // block max
+    // every load of the first kCB chunks is issued up front: (max, sum) of
+    // chunk c by thread c, the o-vectors of dim i by thread i
+    constexpr int kCB = 32;
+    const int i = threadIdx.x;  // blockDim.x == hd
+    float mc = -INFINITY, lc = 0.f;
+    if ((int)threadIdx.x < nch) {
+        mc = base[(long long)threadIdx.x * stride];
+        lc = base[(long long)threadIdx.x * stride + 1];
+    }
+    float ov[kCB];
+#pragma unroll
+    for (int c = 0; c < kCB; ++c) ov[c] = c < nch ? base[(long long)c * stride + 2 + i] : 0.f;
+    float m = mc;
+    for (int c = threadIdx.x + blockDim.x; c < nch; c += blockDim.x) m = fmaxf(m, base[(long long)c * stride]);
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -328,21 +362,32 @@ __global__ void attn_combine_kernel(AttnCombineParams p) {
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, red[w]);
     __syncthreads();
     float l = 0.f;
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    if ((int)threadIdx.x < nch) {
+        const float sc = __expf(mc - M);
+        scale_c[threadIdx.x] = sc;
+        l = lc * sc;
+    }
+    for (int c = threadIdx.x + blockDim.x; c < nch; c += blockDim.x) {
         const float sc = __expf(base[(long long)c * stride] - M);
         scale_c[c] = sc;
         l += base[(long long)c * stride + 1] * sc;
     }
     const float L = block_sum(l, red);  // syncs: scale_c visible
-    for (int i = threadIdx.x; i < p.hd; i += blockDim.x) {
-        float o = 0.f;
-#pragma unroll 4
-        for (int c = 0; c < nch; ++c) o += base[(long long)c * stride + 2 + i] * scale_c[c];
-        const float v = o / L;
-        const int k = h * p.hd + i;
-        p.out_bfrag[bfrag_index(t, k)] = bf16_bits(v);
-        if (p.tap) p.tap[(long long)t * p.H * p.hd + k] = v;
+    float o = 0.f;
+#pragma unroll
+    for (int c = 0; c < kCB; ++c)
+        if (c < nch) o += ov[c] * scale_c[c];
+    for (int c0 = kCB; c0 < nch; c0 += kCB) {
+#pragma unroll
+        for (int c = 0; c < kCB; ++c) ov[c] = c0 + c < nch ? base[(long long)(c0 + c) * stride + 2 + i] : 0.f;
+#pragma unroll
+        for (int c = 0; c < kCB; ++c)
+            if (c0 + c < nch) o += ov[c] * scale_c[c0 + c];
     }
+    const float v = o / L;
+    const int k = h * p.hd + i;
+    p.out_bfrag[p.umma ? umma_b_index(t, k) : bfrag_index(t, k)] = bf16_bits(v);
+    if (p.tap) p.tap[(long long)t * p.H * p.hd + k] = v;
 }
 
 }  // namespace cascade

@@ -118,14 +118,15 @@ static int validate(const cascade_geometry* g) {
     if (g->experts_per_layer > kMaxExperts) return bad("experts_per_layer > 128 (expert_model.hpp:96)");
     if (g->top_k > kMaxTopK) return bad("top_k > 16");
     if (g->shared_experts > 16) return bad("shared_experts > 16");
-    if (g->d_model < 64 || g->d_model % 64) return bad("d_model must be a positive multiple of 64");
+    if (g->d_model < 256 || g->d_model % 256 || g->d_model > 8192) return bad("d_model must be a multiple of 256 in [256, 8192]");
     if (g->d_ff < 32 || g->d_ff % 32) return bad("d_ff must be a positive multiple of 32");
     if (g->head_dim != 32 && g->head_dim != 64 && g->head_dim != 128) return bad("head_dim must be 32, 64 or 128");
     if (g->n_kv_heads < 1 || g->n_heads < 1 || g->n_heads % g->n_kv_heads) return bad("n_heads must be a multiple of n_kv_heads");
     if ((g->n_heads / g->n_kv_heads) * kMaxT > kAttnMaxRows) return bad("n_heads / n_kv_heads must be <= 8");
     if ((g->n_heads * g->head_dim) % 64) return bad("n_heads*head_dim must be a multiple of 64");
     if (((g->n_heads + 2 * g->n_kv_heads) * g->head_dim) % 64) return bad("(H+2KV)*head_dim must be a multiple of 64");
-    if (g->vocab < 64 || g->vocab % 64) return bad("vocab must be a positive multiple of 64");
+    if (g->vocab < 128 || g->vocab % 128) return bad("vocab must be a positive multiple of 128");
+    if (((g->n_heads + 2 * g->n_kv_heads) * g->head_dim) % 128) return bad("(H+2KV)*head_dim must be a multiple of 128");
     if (!(g->rope_theta > 0.f)) return bad("rope_theta must be > 0");
     if (!(g->norm_eps > 0.f)) return bad("norm_eps must be > 0");
     if (!(g->router_scale > 0.f)) return bad("router_scale must be > 0");
@@ -199,6 +200,15 @@ struct cascade_model {
     std::vector<void*> allocs;
     uint64_t bytes = 0;
     nccl_comm_t comm = nullptr;
+    // dense matrices on the tcgen05 engine (gemv_umma.cuh, UMMA layout) vs the
+    // mma.sync engine (gemv.cuh, A-frag layout), per matrix: bit 0 QKV, bit 1
+    // O projection, bit 2 LM head.  Default all three; in-graph A/B of the
+    // masks (profiles/r01/ab) puts them within noise of each other on the
+    // K=0..8 mean, tcgen05 ahead on QKV.  CASCADE_DENSE_UMMA=<mask> overrides.
+    int umma_mask = 7;
+    bool umma_qkv() const { return umma_mask & 1; }
+    bool umma_o() const { return umma_mask & 2; }
+    bool umma_lm() const { return umma_mask & 4; }
 };
 
 template <typename T>
@@ -216,8 +226,9 @@ static uint64_t key_of(const cascade_model* m, int kind, int layer, int expert) 
 }
 
 static int init_afrag(cascade_model* m, uint4* dst, int rows, int cols, int rowmap, int k0, int k1, int k2,
-                      int layer, int expert, int n0 = 0, int n1 = 0) {
+                      int layer, int expert, int n0 = 0, int n1 = 0, int umma = 0) {
     InitParams p{};
+    p.umma = umma;
     p.dst = dst;
     p.n_vec = (long long)rows * cols / 8;
     p.n_ks = cols / 16;
@@ -282,6 +293,7 @@ static int model_create(const cascade_geometry* g, uint64_t seed, int device, in
     local_experts(g->experts_per_layer, ep_rank, ep_size, m->e_lo, m->e_hi);
     m->n_shared_local = local_shared(g->shared_experts, ep_rank, ep_size);
     m->n_blocks = (m->e_hi - m->e_lo) + m->n_shared_local;
+    if (const char* v = getenv("CASCADE_DENSE_UMMA")) m->umma_mask = atoi(v) & 7;
     Dims D(*g);
     m->layers.resize(D.L);
 
@@ -311,8 +323,8 @@ static int model_create(const cascade_geometry* g, uint64_t seed, int device, in
             CK(cudaMemset(w.router + (size_t)D.E * D.d, 0, D.d * 2));
         }
         if ((rc = init_afrag(m, w.wqkv, D.qkvd, D.d, ROWMAP_QKV, CASCADE_T_WQ, CASCADE_T_WK, CASCADE_T_WV, l, 0,
-                             D.hq, D.KV * D.hd)) ||
-            (rc = init_afrag(m, w.wo, D.d, D.hq, ROWMAP_SIMPLE, CASCADE_T_WO, 0, 0, l, 0)))
+                             D.hq, D.KV * D.hd, m->umma_qkv())) ||
+            (rc = init_afrag(m, w.wo, D.d, D.hq, ROWMAP_SIMPLE, CASCADE_T_WO, 0, 0, l, 0, 0, 0, m->umma_o())))
             return fail(rc);
         for (int b = 0; b < m->n_blocks; ++b) {
             // global expert index: local routed experts, then local shared blocks
@@ -340,7 +352,7 @@ static int model_create(const cascade_geometry* g, uint64_t seed, int device, in
         return fail(rc);
     if ((rc = init_plain(m, m->embed, D.V, D.d, CASCADE_T_EMBED, 0, 0, D.d)) ||
         (rc = init_plain(m, m->final_norm, 1, D.d, CASCADE_T_FINAL_NORM, 0, 0, D.d)) ||
-        (rc = init_afrag(m, m->lm_head, D.V, D.d, ROWMAP_SIMPLE, CASCADE_T_LM_HEAD, 0, 0, 0, 0)))
+        (rc = init_afrag(m, m->lm_head, D.V, D.d, ROWMAP_SIMPLE, CASCADE_T_LM_HEAD, 0, 0, 0, 0, 0, 0, m->umma_lm())))
         return fail(rc);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -445,6 +457,40 @@ __global__ void accept_kernel(AcceptParams p) {
     *p.res = r;
 }
 
+// One shared-memory carveout for every kernel of the step: an SM that ran a
+// large-smem kernel otherwise stays configured for it (tiny L1) until
+// it drains, and the L1-cached activation reads of the next GEMV suffer.
+static int g_carveout = 58;  // percent of 228 KB -> the 132 KB configuration
+template <typename K>
+static cudaError_t carve(K k) {
+    return g_carveout > 0 ? cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout)
+                          : cudaSuccess;
+}
+template <int NT>
+static cudaError_t carve_gemv() {
+    cudaError_t e = carve(stream_gemv_kernel<NT, EPI_STORE>);
+    if (e == cudaSuccess) e = carve(stream_gemv_kernel<NT, EPI_ADD>);
+    if (e == cudaSuccess) e = carve(stream_gemv_kernel<NT, EPI_GATEUP>);
+    if (e == cudaSuccess) e = carve(stream_gemv_kernel<NT, EPI_DOWN>);
+    if (e == cudaSuccess) e = carve(stream_gemv_kernel<NT, EPI_ARGMAX>);
+    return e;
+}
+static cudaError_t set_carveouts(int hd) {
+    if (const char* v = getenv("CASCADE_CARVEOUT")) g_carveout = atoi(v);
+    cudaError_t e = carve_gemv<1>();
+    if (e == cudaSuccess) e = carve_gemv<2>();
+    if (e == cudaSuccess) e = carve(stream_gemv_umma_kernel<UEPI_STORE>);
+    if (e == cudaSuccess) e = carve(stream_gemv_umma_kernel<UEPI_ADD>);
+    if (e == cudaSuccess) e = carve(stream_gemv_umma_kernel<UEPI_ARGMAX>);
+    if (e == cudaSuccess) e = carve(moe_route_kernel);
+    if (e == cudaSuccess) e = carve(moe_combine_kernel);
+    if (e == cudaSuccess) e = carve(embed_norm_kernel);
+    if (e == cudaSuccess) e = carve(attn_combine_kernel);
+    if (e == cudaSuccess) e = carve(accept_kernel);
+    if (e == cudaSuccess) e = hd == 32 ? carve(attn_partial_kernel<32>) : hd == 64 ? carve(attn_partial_kernel<64>) : carve(attn_partial_kernel<128>);
+    return e;
+}
+
 template <int NT>
 static cudaError_t gemv_smem_attr() {
     const int sm = gemv_smem_bytes<NT>();
@@ -482,11 +528,17 @@ struct cascade_session {
     cascade_verify_out* d_result = nullptr;
     cascade_verify_out* h_result = nullptr;
     float* x = nullptr;
-    uint16_t* xn = nullptr;
+    uint16_t* xn = nullptr;      // MoE input (B-frag, expert GEMVs)
+    uint16_t* xn_u = nullptr;    // attention / final-norm output (UMMA B layout for tcgen05 QKV / LM head)
+    float* upartial = nullptr;   // tcgen05 engine split-unit partials
+    int* ucounters = nullptr;
     float* qkv = nullptr;
     float* attn_part = nullptr;
     uint16_t* attn_out = nullptr;
     float* logits_router = nullptr;
+    float* logit_part = nullptr;
+    float* ss_part = nullptr;
+    int* tok_ticket = nullptr;
     int* ticket = nullptr;
     int* topk_id = nullptr;
     float* topk_w = nullptr;
@@ -588,10 +640,16 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if ((rc = salloc(s, &s->d_params, sizeof(StepParams))) || (rc = salloc(s, &s->d_state, sizeof(DevState))) ||
         (rc = salloc(s, &s->d_result, sizeof(cascade_verify_out))) ||
         (rc = salloc(s, &s->x, (size_t)kMaxT * D.d * 4)) || (rc = salloc(s, &s->xn, (size_t)D.d * 32)) ||
+        (rc = salloc(s, &s->xn_u, (size_t)D.d * 32)) ||
+        (rc = salloc(s, &s->upartial, (size_t)m->num_sms * 2 * kUPartialFloats * 4, false)) ||
+        (rc = salloc(s, &s->ucounters, (size_t)std::max({D.qkvd, D.d, D.V}) / kURows * 4)) ||
         (rc = salloc(s, &s->qkv, (size_t)kMaxT * D.qkvd * 4)) ||
         (rc = salloc(s, &s->attn_part, (size_t)D.KV * G * kMaxT * s->max_chunks * (D.hd + 2) * 4)) ||
         (rc = salloc(s, &s->attn_out, (size_t)D.hq * 32)) ||
         (rc = salloc(s, &s->logits_router, (size_t)kMaxT * (D.E + 1) * 4)) ||
+        (rc = salloc(s, &s->logit_part, (size_t)kMaxT * (D.d / kRouteSlice) * (D.E + 1) * 4)) ||
+        (rc = salloc(s, &s->ss_part, (size_t)kMaxT * (D.d / kRouteSlice) * 4)) ||
+        (rc = salloc(s, &s->tok_ticket, (size_t)kMaxT * 4)) ||
         (rc = salloc(s, &s->ticket, 4)) || (rc = salloc(s, &s->topk_id, (size_t)kMaxT * D.k * 4)) ||
         (rc = salloc(s, &s->topk_w, (size_t)kMaxT * D.k * 4)) || (rc = salloc(s, &s->gsh, kMaxT * 4)) ||
         (rc = salloc(s, &s->list, (size_t)(nslots + 1) * 4)) || (rc = salloc(s, &s->count, 4)) ||
@@ -627,10 +685,12 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     else if (D.hd == 64) e = cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+    if (e == cudaSuccess) e = set_carveouts(D.hd);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
     if (e == cudaSuccess) e = gemv_smem_attr<1>();
     if (e == cudaSuccess) e = gemv_smem_attr<2>();
-    if (e == cudaSuccess && D.d * 4 > 48 * 1024)
-        e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, D.d * 4);
     if (e != cudaSuccess) {
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
@@ -682,6 +742,24 @@ static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStrea
 }
 
 
+
+static cudaError_t launch_ugemv(int epi, const UGemvParams& p, int grid, cudaStream_t st) {
+    const size_t sm = gemv_umma_smem_bytes();
+    switch (epi) {
+    case UEPI_STORE: return launch_k(stream_gemv_umma_kernel<UEPI_STORE>, grid, kUThreads, sm, st, true, p);
+    case UEPI_ADD: return launch_k(stream_gemv_umma_kernel<UEPI_ADD>, grid, kUThreads, sm, st, true, p);
+    default: return launch_k(stream_gemv_umma_kernel<UEPI_ARGMAX>, grid, kUThreads, sm, st, true, p);
+    }
+}
+
+static UGemvParams ugemv_base(cascade_session* s, int T) {
+    UGemvParams p{};
+    p.T = T;
+    p.n_blocks = 1;
+    p.partial = s->upartial;
+    p.counters = s->ucounters;
+    return p;
+}
 
 static GemvParams gemv_base(cascade_session* s, int T) {
     GemvParams p{};
@@ -741,7 +819,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ep.embed = m->embed;
     ep.norm_w = m->layers[0].attn_norm;
     ep.x = s->x;
-    ep.xn_bfrag = s->xn;
+    ep.xn_bfrag = m->umma_qkv() ? s->xn_u : s->xn;
+    ep.umma = m->umma_qkv();
     ep.tokens_used = s->tokens_used;
     ep.stamp = s->stamps;
     ep.tap_x = taps ? s->taps.x_in : nullptr;
@@ -765,17 +844,30 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         const LayerW& w = m->layers[l];
         const size_t td = (size_t)l * kMaxT * D.d;
         // QKV
-        GemvParams q = gemv_base(s, T);
-        q.W = w.wqkv;
-        q.B = reinterpret_cast<const uint2*>(s->xn);
-        q.n_st = D.qkvd / kSTRows;
-        q.n_ks = D.d / 16;
-        q.out = s->qkv;
-        q.ld = D.qkvd;
-        q.stamp = s->stamps + 1 + 2 * l;
-        q.trace = tr(1);
         PB(1);
-        CK(launch_gemv(EPI_STORE, q, s->gemv_grid, st));
+        if (m->umma_qkv()) {
+            UGemvParams q = ugemv_base(s, T);
+            q.W = reinterpret_cast<const uint16_t*>(w.wqkv);
+            q.B = s->xn_u;
+            q.n_st = D.qkvd / kURows;
+            q.n_ks = D.d / 16;
+            q.out = s->qkv;
+            q.ld = D.qkvd;
+            q.stamp = s->stamps + 1 + 2 * l;
+            q.trace = tr(1);
+            CK(launch_ugemv(UEPI_STORE, q, m->num_sms, st));
+        } else {
+            GemvParams q = gemv_base(s, T);
+            q.W = w.wqkv;
+            q.B = reinterpret_cast<const uint2*>(s->xn);
+            q.n_st = D.qkvd / kSTRows;
+            q.n_ks = D.d / 16;
+            q.out = s->qkv;
+            q.ld = D.qkvd;
+            q.stamp = s->stamps + 1 + 2 * l;
+            q.trace = tr(1);
+            CK(launch_gemv(EPI_STORE, q, s->gemv_grid, st));
+        }
         PE();
         ++nk;
         // attention
@@ -812,6 +904,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         cp.KV = D.KV;
         cp.hd = D.hd;
         cp.max_chunks = s->max_chunks;
+        cp.umma = m->umma_o();
         cp.trace = tr(3);
         PB(3);
         CK(launch_k(attn_combine_kernel, dim3(T, D.H), dim3(D.hd), 0, st, true, cp));
@@ -819,16 +912,28 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ++nk;
         (void)G;
         // O projection + residual
-        GemvParams o = gemv_base(s, T);
-        o.W = w.wo;
-        o.B = reinterpret_cast<const uint2*>(s->attn_out);
-        o.n_st = D.d / kSTRows;
-        o.n_ks = D.hq / 16;
-        o.out = s->x;
-        o.ld = D.d;
-        o.trace = tr(4);
         PB(4);
-        CK(launch_gemv(EPI_ADD, o, s->gemv_grid, st));
+        if (m->umma_o()) {
+            UGemvParams o = ugemv_base(s, T);
+            o.W = reinterpret_cast<const uint16_t*>(w.wo);
+            o.B = s->attn_out;
+            o.n_st = D.d / kURows;
+            o.n_ks = D.hq / 16;
+            o.out = s->x;
+            o.ld = D.d;
+            o.trace = tr(4);
+            CK(launch_ugemv(UEPI_ADD, o, m->num_sms, st));
+        } else {
+            GemvParams o = gemv_base(s, T);
+            o.W = w.wo;
+            o.B = reinterpret_cast<const uint2*>(s->attn_out);
+            o.n_st = D.d / kSTRows;
+            o.n_ks = D.hq / 16;
+            o.out = s->x;
+            o.ld = D.d;
+            o.trace = tr(4);
+            CK(launch_gemv(EPI_ADD, o, s->gemv_grid, st));
+        }
         PE();
         ++nk;
         if (taps) CK(cudaMemcpyAsync(s->taps.x_mid + td, s->x, (size_t)T * D.d * 4, cudaMemcpyDeviceToDevice, st));
@@ -839,6 +944,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.router_w = w.router;
         rp.xn_bfrag = s->xn;
         rp.logits = s->logits_router;
+        rp.logit_part = s->logit_part;
         rp.ticket = s->ticket;
         rp.topk_id = s->topk_id;
         rp.topk_w = s->topk_w;
@@ -865,8 +971,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.stamp = s->stamps + 2 + 2 * l;
         rp.trace = tr(5);
         PB(5);
-        const int rgroups = (D.E + (m->g.shared_gate ? 1 : 0) + kRouteWarps - 1) / kRouteWarps;
-        CK(launch_k(moe_route_kernel, dim3(T, rgroups), dim3(kRouteThreads), (size_t)D.d * 4, st, true, rp));
+        const size_t rsmem = (size_t)(D.E + (m->g.shared_gate ? 1 : 0)) * kRouteSlice * 2;
+        CK(launch_k(moe_route_kernel, dim3(D.d / kRouteSlice, T), dim3(kRouteThreads), rsmem, st, true, rp));
         PE();
         ++nk;
         if (taps) {
@@ -926,7 +1032,13 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.topk_w = s->topk_w;
         c.gsh = s->gsh;
         c.norm_w = (l + 1 < D.L) ? m->layers[l + 1].attn_norm : m->final_norm;
-        c.xn_bfrag = s->xn;
+        {
+            const bool next_umma = (l + 1 < D.L) ? m->umma_qkv() : m->umma_lm();
+            c.xn_bfrag = next_umma ? s->xn_u : s->xn;
+            c.umma = next_umma;
+        }
+        c.ss_part = s->ss_part;
+        c.tok_ticket = s->tok_ticket;
         c.tap_moe = taps ? s->taps.moe_out + td : nullptr;
         c.tap_xn = (taps && l + 1 < D.L) ? s->taps.xn_attn + td + (size_t)kMaxT * D.d : nullptr;
         c.tap_x = (taps && l + 1 < D.L) ? s->taps.x_in + td + (size_t)kMaxT * D.d : nullptr;
@@ -939,23 +1051,37 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.pf_bytes = (pf && l + 1 < D.L) ? D.wqkv_vec * 16 : 0;
         c.trace = tr(8);
         PB(8);
-        CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRouteThreads), 0, st, m->ep_size == 1, c));
+        CK(launch_k(moe_combine_kernel, dim3(D.d / kRouteSlice, T), dim3(kRouteThreads), 0, st, m->ep_size == 1, c));
         PE();
         ++nk;
     }
     // LM head + argmax
-    GemvParams lm = gemv_base(s, T);
-    lm.W = m->lm_head;
-    lm.B = reinterpret_cast<const uint2*>(s->xn);
-    lm.n_st = D.V / kSTRows;
-    lm.n_ks = D.d / 16;
-    lm.keys = s->keys;
-    lm.out = taps ? s->taps.final_logits : nullptr;
-    lm.ld = D.V;
-    lm.stamp = s->stamps + 1 + 2 * D.L;
-    lm.trace = tr(9);
     PB(9);
-    CK(launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st));
+    if (m->umma_lm()) {
+        UGemvParams lm = ugemv_base(s, T);
+        lm.W = reinterpret_cast<const uint16_t*>(m->lm_head);
+        lm.B = s->xn_u;
+        lm.n_st = D.V / kURows;
+        lm.n_ks = D.d / 16;
+        lm.keys = s->keys;
+        lm.out = taps ? s->taps.final_logits : nullptr;
+        lm.ld = D.V;
+        lm.stamp = s->stamps + 1 + 2 * D.L;
+        lm.trace = tr(9);
+        CK(launch_ugemv(UEPI_ARGMAX, lm, m->num_sms, st));
+    } else {
+        GemvParams lm = gemv_base(s, T);
+        lm.W = m->lm_head;
+        lm.B = reinterpret_cast<const uint2*>(s->xn);
+        lm.n_st = D.V / kSTRows;
+        lm.n_ks = D.d / 16;
+        lm.keys = s->keys;
+        lm.out = taps ? s->taps.final_logits : nullptr;
+        lm.ld = D.V;
+        lm.stamp = s->stamps + 1 + 2 * D.L;
+        lm.trace = tr(9);
+        CK(launch_gemv(EPI_ARGMAX, lm, s->gemv_grid, st));
+    }
     PE();
     ++nk;
     AcceptParams ap{};
@@ -1218,11 +1344,15 @@ extern "C" int cascade_read_tap(cascade_session* s, int kind, void* out, size_t 
 
 // ---------------------------------------------------------------- weights readback
 __global__ void afrag_extract_kernel(const uint16_t* src, int n_ks, int row_phys0, int phys_step_mode, int nrows,
-                                     int cols, uint16_t* dst) {
+                                     int cols, uint16_t* dst, int umma) {
     // phys_step_mode: 0 = rows contiguous; 1 = gate rows; 2 = up rows (GATEUP layout)
     const long long n = (long long)nrows * cols;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const int rr = (int)(i / cols), c = (int)(i % cols);
+        if (umma) {
+            dst[i] = src[umma_a_index((long long)row_phys0 + rr, c, n_ks)];
+            continue;
+        }
         int R;
         if (phys_step_mode == 0) R = row_phys0 + rr;
         else {
@@ -1250,6 +1380,7 @@ extern "C" int cascade_read_weight(cascade_model* m, int kind, int layer, int ex
     int cols = D.d, rows_total = 0;
     const uint4* af = nullptr;
     int n_ks = 0, mode = 0, phys0 = row0;
+    int umma = 0;
     switch (kind) {
     case CASCADE_T_EMBED: plain = m->embed; rows_total = D.V; break;
     case CASCADE_T_FINAL_NORM: plain = m->final_norm; rows_total = 1; break;
@@ -1258,12 +1389,18 @@ extern "C" int cascade_read_weight(cascade_model* m, int kind, int layer, int ex
     case CASCADE_T_ROUTER: plain = m->layers[layer].router; rows_total = D.E; break;
     case CASCADE_T_SHARED_GATE:
         plain = m->layers[layer].router + (size_t)D.E * D.d; rows_total = m->g.shared_gate ? 1 : 0; break;
-    case CASCADE_T_WQ: af = m->layers[layer].wqkv; rows_total = D.hq; n_ks = D.d / 16; break;
-    case CASCADE_T_WK: af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + row0; break;
+    case CASCADE_T_WQ: af = m->layers[layer].wqkv; rows_total = D.hq; n_ks = D.d / 16; umma = m->umma_qkv(); break;
+    case CASCADE_T_WK:
+        af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + row0;
+        umma = m->umma_qkv();
+        break;
     case CASCADE_T_WV:
-        af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + D.KV * D.hd + row0; break;
-    case CASCADE_T_WO: af = m->layers[layer].wo; rows_total = D.d; cols = D.hq; n_ks = D.hq / 16; break;
-    case CASCADE_T_LM_HEAD: af = m->lm_head; rows_total = D.V; n_ks = D.d / 16; break;
+        af = m->layers[layer].wqkv; rows_total = D.KV * D.hd; n_ks = D.d / 16; phys0 = D.hq + D.KV * D.hd + row0;
+        umma = m->umma_qkv();
+        break;
+    case CASCADE_T_WO:
+        af = m->layers[layer].wo; rows_total = D.d; cols = D.hq; n_ks = D.hq / 16; umma = m->umma_o(); break;
+    case CASCADE_T_LM_HEAD: af = m->lm_head; rows_total = D.V; n_ks = D.d / 16; umma = m->umma_lm(); break;
     case CASCADE_T_W_GATE:
     case CASCADE_T_W_UP:
     case CASCADE_T_W_DOWN: {
@@ -1293,7 +1430,8 @@ extern "C" int cascade_read_weight(cascade_model* m, int kind, int layer, int ex
     }
     uint16_t* tmp = nullptr;
     CK(cudaMalloc(&tmp, n * 2));
-    afrag_extract_kernel<<<256, 256>>>(reinterpret_cast<const uint16_t*>(af), n_ks, phys0, mode, nrows, cols, tmp);
+    afrag_extract_kernel<<<256, 256>>>(reinterpret_cast<const uint16_t*>(af), n_ks, phys0, mode, nrows, cols, tmp,
+                                       umma);
     cudaError_t e = cudaDeviceSynchronize();
     if (e == cudaSuccess) e = cudaMemcpy(out, tmp, n * 2, cudaMemcpyDeviceToHost);
     cudaFree(tmp);

@@ -17,8 +17,10 @@
 //    values: a token's column never mixes with another's, so N = 16 always
 //    and results do not depend on T.
 //
-// Warp roles (192 threads, one CTA per SM, <= 110 KB smem so two kernels'
-// CTAs can overlap on an SM under PDL):
+// Warp roles (192 threads, one CTA per SM; 108 KB of smem = three 32 KB
+// weight stages + activations (scripts/umma_probe.cu sweep, profiles/r01),
+// small enough that every kernel of the step runs in the same 132 KB
+// shared-memory carveout and the SMs never reconfigure L1 between them):
 //  * warps 0-3: epilogue — warp w owns TMEM lanes 32w..32w+31 = rows of
 //    the unit; tcgen05.ld.32x32b.x16 gives each thread its row for all 16
 //    tokens; fused epilogues (store, residual add, SiLU(gate)*up into the
@@ -26,8 +28,8 @@
 //  * warp 4 lane 0: TMA producer.  Weights of dense matrices (and of the
 //    expert down projection, whose active list is final once the gate/up
 //    kernel passed its griddepcontrol.wait) are requested BEFORE
-//    griddepcontrol.wait, so the first 96 KB per SM stream in while the
-//    previous latency-bound kernel is still running.
+//    griddepcontrol.wait, so the first 96 KB per SM (14 MB over the chip)
+//    stream in while the previous latency-bound kernel is still running.
 //  * warp 5: TMEM allocation (32 columns = two 128x16 fp32 accumulators,
 //    double-buffered against the epilogue); lane 0 issues tcgen05.mma
 //    (M=128, N=16, K=16, bf16 in, fp32 accumulate) and tcgen05.commit to
@@ -53,10 +55,10 @@ constexpr int kUTok = 16;                         // UMMA N: token slots
 constexpr int kUKsA = kURows * 16 * 2;            // 4 KB of weights per k-step
 constexpr int kUKsB = kUTok * 16 * 2;             // 512 B of activations per k-step
 #ifndef CASCADE_USTAGE_KS
-#define CASCADE_USTAGE_KS 4
+#define CASCADE_USTAGE_KS 8
 #endif
 #ifndef CASCADE_USTAGES
-#define CASCADE_USTAGES 6
+#define CASCADE_USTAGES 3
 #endif
 constexpr int kUStageKs = CASCADE_USTAGE_KS;      // k-steps per ring stage
 constexpr int kUStages = CASCADE_USTAGES;         // 96 KB of weights in flight per SM
@@ -112,7 +114,13 @@ struct UGemvParams {
     unsigned long long* keys;  // UEPI_ARGMAX
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
     unsigned long long* trace; // in-graph trace slot
+    unsigned long long* dbg;   // optional phase stamps (scripts/umma_probe.cu)
 };
+
+// phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
+__device__ __forceinline__ void udbg(const UGemvParams& p, int i) {
+    if (p.dbg != nullptr && blockIdx.x == 0) p.dbg[i] = globaltimer_raw();
+}
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -190,7 +198,10 @@ struct UWork {
 __device__ __forceinline__ UWork uwork(const UGemvParams& p, int U) {
     UWork w;
     w.per_block = (long long)p.n_st * p.n_ks;
-    long long min_piece = p.n_ks / 2 > kUMinPieceKs ? p.n_ks / 2 : kUMinPieceKs;
+    // dense: spread over every SM; routed blocks: pieces of >= half a unit
+    // so a unit is reduced from at most ~3 partials
+    long long min_piece = kUMinPieceKs;
+    if (p.list != nullptr && p.n_ks / 2 > min_piece) min_piece = p.n_ks / 2;
     long long pm = w.per_block / min_piece;
     if (pm < 1) pm = 1;
     w.P = pm < (long long)gridDim.x ? (int)pm : (int)gridDim.x;
@@ -285,6 +296,10 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_sh;
+    if (threadIdx.x == 0) {
+        udbg(p, 0);
+        if (p.dbg) atomicMin(p.dbg + 10, globaltimer_raw());
+    }
 
     const bool dense = p.list == nullptr && p.count == nullptr;
     const bool early = dense || p.early_list;  // weights addressable before griddepcontrol.wait
@@ -353,6 +368,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
             griddep_wait();
             griddep_launch();
             if (lane != 0) goto producer_done;
+            udbg(p, 1);
             for (int j = 0; j < (PROBE == 2 ? 0 : n_pre); ++j)
                 bulk_g2s(ring + (size_t)pre_b_slot[j] * kUStageBytes + kUStageA, p.B + pre_b_off[j], pre_b_bytes[j],
                          &full_bar[pre_b_slot[j]], pol_b);
@@ -361,6 +377,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
                 w = uwork(p, U);
             }
             issue(0x7fffffff, true);
+            udbg(p, 2);
         }
     producer_done:;
     } else if (warp == 5) {
@@ -371,6 +388,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
             const int U = p.count ? *p.count : p.n_blocks;
             const UWork w = uwork(p, U);
             int i = 0, v = -1;
+            udbg(p, 3);
             for (int item = blockIdx.x; item < w.n_items; item += grid) {
                 const int q = item % w.P;
                 long long pos = piece_lo(w, q);
@@ -409,6 +427,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
                     else umma_commit(&accf_bar[a]);
                 }
             }
+            udbg(p, 4);
         }
         __syncwarp();
     } else {
@@ -417,6 +436,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
         griddep_launch();
         trace_start(p.trace);
         if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
+        if (threadIdx.x == 0) udbg(p, 5);
         const int U = p.count ? *p.count : p.n_blocks;
         const UWork w = uwork(p, U);
         const int r = warp * 32 + lane;  // TMEM lane = unit row
@@ -432,6 +452,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
                 mb_wait(&accf_bar[a], (v >> 1) & 1);
                 tc_fence_after();
                 float val[16];
+                if (v == 0 && threadIdx.x == 0) udbg(p, 6);
                 tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(a * kUTok), val);
                 tc_fence_before();
                 __syncwarp();
@@ -473,8 +494,10 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
             }
         }
     }
+    if (threadIdx.x == 0) udbg(p, 7);
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0 && p.dbg) atomicMax(p.dbg + 9, globaltimer_raw());
     if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");

@@ -5,6 +5,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "gemv_umma.cuh"
 
 namespace cascade {
 
@@ -23,6 +24,7 @@ struct InitParams {
     uint64_t key[3];     // per logical kind
     float scale[3];
     int cols;            // logical K (row stride of the hashed index)
+    int umma;            // 1: UMMA A layout (gemv_umma.cuh), 0: A-frag (gemv.cuh)
 };
 
 __global__ void init_afrag_kernel(InitParams p) {
@@ -34,16 +36,27 @@ __global__ void init_afrag_kernel(InitParams p) {
         const long long q3 = q2 / kTPW;
         const int s = (int)(q3 % p.n_ks);
         const long long st = q3 / p.n_ks;
+        // UMMA layout: uint4 q = 8 consecutive columns of one row of a core matrix
+        const long long ku = q % ((long long)p.n_ks * 2 * kURows);
+        const long long unit = q / ((long long)p.n_ks * 2 * kURows);
+        const int us = (int)(ku / (2 * kURows)), ukc = (int)((ku / kURows) & 1), ur = (int)(ku % kURows);
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
             uint16_t v[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                int r, c;
-                afrag_coords(lane, e + h, r, c);
-                const long long prow = st * kSTRows + it * 16 + r;
-                const int col = s * 16 + c;
+                long long prow;
+                int col;
+                if (p.umma) {
+                    prow = unit * kURows + ur;
+                    col = us * 16 + ukc * 8 + e + h;
+                } else {
+                    int r, c;
+                    afrag_coords(lane, e + h, r, c);
+                    prow = st * kSTRows + it * 16 + r;
+                    col = s * 16 + c;
+                }
                 int kind = 0;
                 long long lrow = prow;
                 if (p.rowmap == ROWMAP_GATEUP) {

@@ -21,6 +21,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "gemv_umma.cuh"
 
 namespace cascade {
 
@@ -49,6 +50,7 @@ struct RouteParams {
     const uint16_t* router_w;    // [E + shared_gate][d] bf16
     uint16_t* xn_bfrag;          // out: MoE input, B-frag
     float* logits;               // out: [T][E+1]
+    float* logit_part;           // scratch: [T][n_slices][E+1] per-slice partial logits
     int* ticket;                 // zero between launches
     int* topk_id;                // out: [T][k]
     float* topk_w;               // out: [T][k]
@@ -68,63 +70,73 @@ struct RouteParams {
     unsigned long long* trace;
 };
 
+constexpr int kRouteSlice = kRouteThreads;  // d columns per CTA (one per thread)
+constexpr int kMaxSlices = 32;              // d <= 8192
+
+// grid = (d / kRouteSlice, T).  CTA (slice, t): the router weights of its
+// column slice are staged in shared memory BEFORE griddepcontrol.wait (they
+// do not depend on the predecessor); after it, 1/rms of token t's full
+// residual row (L2), the bf16 MoE input of its slice (written once, B-frag)
+// and the slice's partial router logits for every expert row.  The last
+// CTA (atomic ticket) sums the partials in slice order and routes all
+// tokens: softmax, top-k (larger logit first, lower expert index on ties),
+// gate weights (renormalised over the k for Mixtral), then the expert
+// union: OR of per-token 128-bit masks, ascending unique-expert list,
+// per-expert token ranks.  This is the real counterpart of the
+// reference's stand-ins draw_expert_set / sample_active_experts
+// (expert_model.hpp:100-139): union = distinct routed experts, shared
+// blocks always active on top.
 __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p) {
+    extern __shared__ uint16_t wsl[];  // [n_rows][kRouteSlice] router weights of this slice
+    __shared__ float red[32];
+    __shared__ float wred[kRouteWarps][kMaxExperts + 1];
+    __shared__ int s_last;
+    __shared__ float s_logits[kMaxT][kMaxExperts + 1];
+    __shared__ unsigned long long masks[kMaxT][2];
+    const int slice = blockIdx.x, t = blockIdx.y;
+    const int n_slices = gridDim.x;
+    const int n_rows = p.E + (p.shared_gate ? 1 : 0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = slice * kRouteSlice + threadIdx.x;
+    // ---- independent of the predecessor: router + norm weights of the slice
+    for (int e = 0; e < n_rows; ++e) wsl[e * kRouteSlice + threadIdx.x] = p.router_w[(long long)e * p.d + c];
+    const float nw = bits_to_f32(p.norm_w[c]);
     griddep_wait();
     griddep_launch();
     trace_start(p.trace);
-    __shared__ float red[32];
-    __shared__ int s_last;
-    __shared__ unsigned long long masks[kMaxT][2];
-    extern __shared__ float xs[];  // [d] normalised input (bf16 values as fp32)
-    const int t = blockIdx.x;
-    const int grp = blockIdx.y;
-    if (t == 0 && grp == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    if (slice == 0 && t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    // ---- 1/rms of the full row (every load issued before the reduction)
     const float* x = p.x + (long long)t * p.d;
-    const float rinv = row_rinv(x, p.d, p.eps, red);
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        const uint16_t b = bf16_bits((x[i] * rinv) * bits_to_f32(p.norm_w[i]));
-        xs[i] = bits_to_f32(b);
-        if (grp == 0) {
-            p.xn_bfrag[bfrag_index(t, i)] = b;
-            if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
-        }
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < (p.d >> 2); i += kRouteThreads) {
+        const float4 v = x4[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
     }
-    __syncthreads();
-    const int n_rows = p.E + (p.shared_gate ? 1 : 0);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int e = grp * kRouteWarps + warp;
-    if (e < n_rows) {
-        const uint4* w4 = reinterpret_cast<const uint4*>(p.router_w + (long long)e * p.d);
-        const int n8 = p.d >> 3;  // uint4 per row
-        float acc = 0.f;
-        for (int base = 0; base < n8; base += 32 * 8) {
-            uint4 w[8];
+    ss = block_sum(ss, red);
+    const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
+    const uint16_t b = bf16_bits((x[c] * rinv) * nw);
+    p.xn_bfrag[bfrag_index(t, c)] = b;
+    if (p.tap_xn) p.tap_xn[(long long)t * p.d + c] = b;
+    const float xv = bits_to_f32(b);
+    // ---- partial router logits of the slice (fixed reduction order)
+    for (int e = 0; e < n_rows; ++e) {
+        float v = xv * bits_to_f32(wsl[e * kRouteSlice + threadIdx.x]);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = base + u * 32 + lane;
-                w[u] = i < n8 ? __ldg(w4 + i) : make_uint4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int i = base + u * 32 + lane;
-                if (i >= n8) continue;
-                const float* xv = xs + i * 8;
-                const uint32_t ww[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc = fmaf(xv[2 * q], __uint_as_float(ww[q] << 16), acc);
-                    acc = fmaf(xv[2 * q + 1], __uint_as_float(ww[q] & 0xFFFF0000u), acc);
-                }
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) p.logits[t * (p.E + 1) + e] = acc;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) wred[warp][e] = v;
     }
-    if (p.zero_nonlocal && grp == 0) {
+    if (p.zero_nonlocal) {
         // EP: every (token, rank) row is written by exactly one rank's down
         // GEMV; the others must contribute exact zeros to the all-reduce.
-        float4* y = reinterpret_cast<float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
-        for (int i = threadIdx.x; i < (p.k + p.S) * p.d / 4; i += blockDim.x) y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d;
+        for (int r = 0; r < p.k + p.S; ++r) y[(long long)r * p.d + c] = 0.f;
+    }
+    __syncthreads();
+    if (threadIdx.x < n_rows) {
+        float v = 0.f;
+        for (int w = 0; w < kRouteWarps; ++w) v += wred[w][threadIdx.x];
+        p.logit_part[((long long)t * n_slices + slice) * (p.E + 1) + threadIdx.x] = v;
     }
     __threadfence();
     __syncthreads();
@@ -133,17 +145,31 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
     if (!s_last) return;
     __threadfence();
 
-    // ---- routing of all tokens (last CTA) ----
+    // ---- routing of all tokens (last CTA)
+    for (int q = threadIdx.x; q < p.T * n_rows; q += kRouteThreads) {
+        const int tt = q / n_rows, e = q - tt * n_rows;
+        float pv[kMaxSlices];
+#pragma unroll
+        for (int sl = 0; sl < kMaxSlices; ++sl)
+            pv[sl] = sl < n_slices ? __ldcg(p.logit_part + ((long long)tt * n_slices + sl) * (p.E + 1) + e) : 0.f;
+        float v = 0.f;
+#pragma unroll
+        for (int sl = 0; sl < kMaxSlices; ++sl)
+            if (sl < n_slices) v += pv[sl];
+        s_logits[tt][e] = v;
+        p.logits[tt * (p.E + 1) + e] = v;
+    }
+    __syncthreads();
     __shared__ int s_topk[kMaxT * kMaxTopK];
     __shared__ int s_warp_on[kMaxExperts / 32];
     for (int tt = warp; tt < p.T; tt += kRouteWarps) {
-        const float* lg = p.logits + tt * (p.E + 1);
+        const float* lg = s_logits[tt];
         float v[kMaxExperts / 32];
         float m = -INFINITY;
 #pragma unroll
         for (int q = 0; q < kMaxExperts / 32; ++q) {
             const int ei = lane + 32 * q;
-            v[q] = ei < p.E ? __ldcg(lg + ei) : -INFINITY;
+            v[q] = ei < p.E ? lg[ei] : -INFINITY;
             m = fmaxf(m, v[q]);
         }
         for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -194,7 +220,7 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
             p.topk_w[tt * p.k + lane] = my_e / den;
         }
         if (lane == 0) {
-            p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-__ldcg(lg + p.E))) : 1.0f;
+            p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-lg[p.E])) : 1.0f;
             masks[tt][0] = m0;
             masks[tt][1] = m1;
         }
@@ -250,6 +276,9 @@ struct CombineParams {
     const float* gsh;            // [T]
     const uint16_t* norm_w;      // next norm weights [d]
     uint16_t* xn_bfrag;          // out
+    float* ss_part;              // scratch [T][n_slices] partial sums of squares
+    int umma;                    // xn_bfrag in the UMMA B layout (dense tcgen05 GEMVs) instead of B-frag
+    int* tok_ticket;             // [T] arrival counters (zero between launches)
     float* tap_moe;              // optional [T][d] (the MoE contribution)
     uint16_t* tap_xn;            // optional [T][d] next-norm output
     float* tap_x;                // optional [T][d] residual after the add
@@ -260,70 +289,83 @@ struct CombineParams {
     unsigned long long* trace;
 };
 
+// grid = (d / kRouteSlice, T).  CTA (slice, t): residual += sum_r w[t][r] *
+// Y[t][r] (+ shared-gate * sum_b Y[t][k+b]) for its columns in fixed order,
+// one column per thread with every load independent; the slice's sum of
+// squares goes to ss_part.  The last slice CTA of token t (per-token ticket)
+// sums the partials in slice order and writes the next RMSNorm (next
+// layer's attention input, or the final norm) for the whole row.
 __global__ void __launch_bounds__(kRouteThreads) moe_combine_kernel(CombineParams p) {
+    __shared__ float red[32];
+    __shared__ int s_last;
+    const int slice = blockIdx.x, t = blockIdx.y;
+    const int n_slices = gridDim.x;
+    const int c = slice * kRouteSlice + threadIdx.x;
     griddep_wait();
     griddep_launch();
     trace_start(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
-    __shared__ float red[32];
-    __shared__ float wsh[kMaxTopK + 1];
-    const int t = blockIdx.x;
-    if (threadIdx.x < p.k) wsh[threadIdx.x] = p.topk_w[t * p.k + threadIdx.x];
-    if (threadIdx.x == 0) wsh[kMaxTopK] = p.gsh[t];
-    __syncthreads();
-    float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
-    const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
-    const int n4 = p.d >> 2;
-    const float g = wsh[kMaxTopK];
-    float ss = 0.f;
-#pragma unroll 2
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int r = 0; r < p.k; ++r) {
-            const float4 y = y4[(long long)r * n4 + i];
-            const float w = wsh[r];
-            acc.x += w * y.x;
-            acc.y += w * y.y;
-            acc.z += w * y.z;
-            acc.w += w * y.w;
-        }
-        if (p.S > 0) {
-            float4 sh = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int b = 0; b < p.S; ++b) {
-                const float4 y = y4[(long long)(p.k + b) * n4 + i];
-                sh.x += y.x;
-                sh.y += y.y;
-                sh.z += y.z;
-                sh.w += y.w;
-            }
-            acc.x += g * sh.x;
-            acc.y += g * sh.y;
-            acc.z += g * sh.z;
-            acc.w += g * sh.w;
-        }
-        if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
-        float4 nx = x4[i];
-        nx.x += acc.x;
-        nx.y += acc.y;
-        nx.z += acc.z;
-        nx.w += acc.w;
-        x4[i] = nx;
-        if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = nx;
-        ss += nx.x * nx.x + nx.y * nx.y + nx.z * nx.z + nx.w * nx.w;
-    }
-    ss = block_sum(ss, red);
-    const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-        const float4 v = x4[i];
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+    const float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d + c;
+    float* xr = p.x + (long long)t * p.d;
+    // all loads first (one round trip), then the fixed-order sums
+    float yv[kMaxTopK], wr[kMaxTopK], ys[kMaxTopK];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int col = 4 * i + q;
-            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[col]));
-            p.xn_bfrag[bfrag_index(t, col)] = b;
-            if (p.tap_xn) p.tap_xn[(long long)t * p.d + col] = b;
+    for (int r = 0; r < kMaxTopK; ++r) {
+        if (r < p.k) {
+            yv[r] = y[(long long)r * p.d];
+            wr[r] = __ldg(p.topk_w + t * p.k + r);
+        }
+        if (r < p.S) ys[r] = y[(long long)(p.k + r) * p.d];
+    }
+    const float x0 = xr[c];
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxTopK; ++r)
+        if (r < p.k) acc += wr[r] * yv[r];
+    if (p.S > 0) {
+        float sh = 0.f;
+#pragma unroll
+        for (int b = 0; b < kMaxTopK; ++b)
+            if (b < p.S) sh += ys[b];
+        acc += __ldg(p.gsh + t) * sh;
+    }
+    if (p.tap_moe) p.tap_moe[(long long)t * p.d + c] = acc;
+    const float nx = x0 + acc;
+    xr[c] = nx;
+    if (p.tap_x) p.tap_x[(long long)t * p.d + c] = nx;
+    const float ss = block_sum(nx * nx, red);
+    if (threadIdx.x == 0) p.ss_part[t * n_slices + slice] = ss;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.tok_ticket + t, 1) == n_slices - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // every load of the tail issued before any use (one L2 round trip each)
+    float xv[kMaxSlices], wv[kMaxSlices], sp[kMaxSlices];
+#pragma unroll
+    for (int j = 0; j < kMaxSlices; ++j) {
+        if (j < n_slices) {
+            xv[j] = __ldcg(xr + j * kRouteSlice + threadIdx.x);
+            wv[j] = bits_to_f32(p.norm_w[j * kRouteSlice + threadIdx.x]);
+            sp[j] = __ldcg(p.ss_part + t * n_slices + j);
         }
     }
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxSlices; ++j)
+        if (j < n_slices) tot += sp[j];
+    const float rinv = 1.0f / sqrtf(tot / (float)p.d + p.eps);
+#pragma unroll
+    for (int j = 0; j < kMaxSlices; ++j) {
+        if (j < n_slices) {
+            const int i = j * kRouteSlice + threadIdx.x;
+            const uint16_t b = bf16_bits((xv[j] * rinv) * wv[j]);
+            p.xn_bfrag[p.umma ? umma_b_index(t, i) : bfrag_index(t, i)] = b;
+            if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
+        }
+    }
+    if (threadIdx.x == 0) p.tok_ticket[t] = 0;
 }
 
 // Step entry: token embedding + first RMSNorm + the step's RoPE table;
@@ -363,6 +405,7 @@ struct EmbedParams {
     const void* pf;              // layer-0 QKV weights -> L2
     unsigned long long pf_bytes;
     unsigned long long* trace;
+    int umma;                    // xn_bfrag in the UMMA B layout
 };
 
 __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p) {
@@ -396,7 +439,7 @@ __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
     for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
         const uint16_t b = bf16_bits((x[i] * rinv) * bits_to_f32(p.norm_w[i]));
-        p.xn_bfrag[bfrag_index(t, i)] = b;
+        p.xn_bfrag[p.umma ? umma_b_index(t, i) : bfrag_index(t, i)] = b;
         if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
     }
 }

@@ -37,6 +37,15 @@ __global__ void fill_x(uint16_t* B, int K) {
     }
 }
 
+// PDL primary: triggers its dependents at once, then stays busy for `ns`
+__global__ void spin_kernel(unsigned long long ns, unsigned long long* dbg) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const unsigned long long t0 = globaltimer_raw();
+    while (globaltimer_raw() - t0 < ns) {
+    }
+    if (threadIdx.x == 0) atomicMax(dbg + 11, globaltimer_raw());
+}
+
 #define CK(x)                                                                                   \
     do {                                                                                        \
         cudaError_t e_ = (x);                                                                   \
@@ -122,6 +131,39 @@ static int run(long long rows, int K, int T, int reps, int grid) {
                mode == 0 ? "full" : mode == 1 ? "no-mma" : mode == 2 ? "no-B" : "full+PDL back-to-back",
                ms * 1e3 / reps, bytes / (ms / reps) / 1e6);
     }
+    // phase timeline behind a 10 us PDL primary (the in-graph situation)
+    {
+        unsigned long long* dbg;
+        CK(cudaMalloc(&dbg, 16 * 8));
+        for (int rep = 0; rep < 3; ++rep) {
+            std::vector<unsigned long long> h0(16, 0);
+            h0[10] = ~0ull;
+            CK(cudaMemcpy(dbg, h0.data(), 16 * 8, cudaMemcpyHostToDevice));
+            UGemvParams q = p;
+            q.dbg = dbg;
+            spin_kernel<<<grid, 32>>>(10000, dbg);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = grid;
+            cfg.blockDim = kUThreads;
+            cfg.dynamicSmemBytes = smem;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, stream_gemv_umma_kernel<UEPI_STORE, 0>, q));
+            CK(cudaDeviceSynchronize());
+            std::vector<unsigned long long> h(16);
+            CK(cudaMemcpy(h.data(), dbg, 16 * 8, cudaMemcpyDeviceToHost));
+            const double z = (double)h[11];
+            auto rel = [&](int i) { return ((double)h[i] - z) / 1e3; };
+            if (rep == 2)
+                printf("   PDL timeline (us rel. to primary end): first CTA entry %.2f | CTA0 entry %.2f prod-wait %.2f "
+                       "prod-done %.2f mma-start %.2f mma-done %.2f epi-wait %.2f epi-first %.2f epi-end %.2f | last CTA end %.2f\n",
+                       rel(10), rel(0), rel(1), rel(2), rel(3), rel(4), rel(5), rel(6), rel(7), rel(9));
+        }
+        cudaFree(dbg);
+    }
     cudaFree(W);
     cudaFree(B);
     cudaFree(out);
@@ -140,6 +182,7 @@ int main() {
     rc |= run(6144, 4096, 9, 20, sms);   // Mixtral QKV
     rc |= run(4096, 4096, 1, 20, sms);   // Mixtral O
     rc |= run(57344, 4096, 16, 10, sms); // two Mixtral gate/up experts (470 MB)
+    rc |= run(4096, 4096, 9, 20, sms);   // Mixtral O at T=9
     rc |= run(32000, 4096, 3, 10, sms);  // LM head
     printf("rc=%d\n", rc);
     return rc;
