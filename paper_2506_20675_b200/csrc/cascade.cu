@@ -151,6 +151,14 @@ struct Dims {
     }
 };
 
+static int g_route_stage = 0;  // CASCADE_ROUTE_STAGE=1: stage router weights in smem (A/B: off measured faster)
+static bool route_staged(const Dims& D, int shared_gate) {
+    return g_route_stage && (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2 <= (size_t)kRouteStageBytes;
+}
+static size_t route_smem_bytes(const Dims& D, int shared_gate) {
+    return (size_t)D.d * 4 + (route_staged(D, shared_gate) ? (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2 : 0);
+}
+
 static void local_experts(int E, int rank, int size, int& lo, int& hi) {
     lo = (int)((long long)E * rank / size);
     hi = (int)((long long)E * (rank + 1) / size);
@@ -686,6 +694,11 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     else if (D.hd == 64) e = cudaFuncSetAttribute(attn_partial_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     if (e == cudaSuccess) e = set_carveouts(D.hd);
+    if (const char* v = getenv("CASCADE_ROUTE_STAGE")) g_route_stage = atoi(v);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)route_smem_bytes(D, m->g.shared_gate));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
     if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
@@ -742,6 +755,26 @@ static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStrea
 }
 
 
+
+// moe_route_kernel: one thread-block cluster of T CTAs (T <= 16, the
+// non-portable cluster size is opted into at session creation), PDL.
+static cudaError_t launch_route(const RouteParams& p, int T, size_t smem, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(T);
+    cfg.blockDim = dim3(kRowThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = T;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, moe_route_kernel, p);
+}
 
 static cudaError_t launch_ugemv(int epi, const UGemvParams& p, int grid, cudaStream_t st) {
     const size_t sm = gemv_umma_smem_bytes();
@@ -968,11 +1001,11 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.ep_size = m->ep_size;
         rp.eps = m->g.norm_eps;
         rp.zero_nonlocal = m->ep_size > 1;
+        rp.stage_w = route_staged(D, m->g.shared_gate);
         rp.stamp = s->stamps + 2 + 2 * l;
         rp.trace = tr(5);
         PB(5);
-        const size_t rsmem = (size_t)(D.E + (m->g.shared_gate ? 1 : 0)) * kRouteSlice * 2;
-        CK(launch_k(moe_route_kernel, dim3(D.d / kRouteSlice, T), dim3(kRouteThreads), rsmem, st, true, rp));
+        CK(launch_route(rp, T, route_smem_bytes(D, m->g.shared_gate), st));
         PE();
         ++nk;
         if (taps) {
@@ -1051,7 +1084,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.pf_bytes = (pf && l + 1 < D.L) ? D.wqkv_vec * 16 : 0;
         c.trace = tr(8);
         PB(8);
-        CK(launch_k(moe_combine_kernel, dim3(D.d / kRouteSlice, T), dim3(kRouteThreads), 0, st, m->ep_size == 1, c));
+        CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRowThreads), 0, st, m->ep_size == 1, c));
         PE();
         ++nk;
     }

@@ -20,6 +20,8 @@
 //   (next layer's attention input, or the final norm).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "gemv_umma.cuh"
 
@@ -66,104 +68,126 @@ struct RouteParams {
     int ep_rank, ep_size;        // shared block b lives on rank b % ep_size
     float eps;
     int zero_nonlocal;
+    int stage_w;                 // router weights staged in smem before griddepcontrol.wait
     unsigned long long* stamp;   // MoE-block start (CostBreakdown split)
     unsigned long long* trace;
 };
 
-constexpr int kRouteSlice = kRouteThreads;  // d columns per CTA (one per thread)
+constexpr int kRouteSlice = kRouteThreads;  // legacy slicing unit (d % 256 == 0)
 constexpr int kMaxSlices = 32;              // d <= 8192
+constexpr int kRowThreads = 512;            // route / combine: one CTA per token row
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
 
-// grid = (d / kRouteSlice, T).  CTA (slice, t): the router weights of its
-// column slice are staged in shared memory BEFORE griddepcontrol.wait (they
-// do not depend on the predecessor); after it, 1/rms of token t's full
-// residual row (L2), the bf16 MoE input of its slice (written once, B-frag)
-// and the slice's partial router logits for every expert row.  The last
-// CTA (atomic ticket) sums the partials in slice order and routes all
-// tokens: softmax, top-k (larger logit first, lower expert index on ties),
-// gate weights (renormalised over the k for Mixtral), then the expert
-// union: OR of per-token 128-bit masks, ascending unique-expert list,
-// per-expert token ranks.  This is the real counterpart of the
-// reference's stand-ins draw_expert_set / sample_active_experts
-// (expert_model.hpp:100-139): union = distinct routed experts, shared
-// blocks always active on top.
-__global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p) {
-    extern __shared__ uint16_t wsl[];  // [n_rows][kRouteSlice] router weights of this slice
+// grid = T CTAs = one thread-block cluster (T <= 16, non-portable size);
+// CTA t = token t = cluster rank t.
+//  * before griddepcontrol.wait (independent of the predecessor): the
+//    router weights (when they fit, e.g. Mixtral's 72 KB) are staged in
+//    shared memory and the norm weights loaded;
+//  * then 1/rms of the token's residual row, the bf16 MoE input (B-frag
+//    for the expert GEMVs, and fp32 in smem), router logits (warp per
+//    expert row, fixed lane order), softmax and top-k (larger logit first,
+//    lower expert index on ties), gate weights (renormalised over the k for
+//    Mixtral);
+//  * cluster barrier; rank 0 gathers every token's top-k and 128-bit
+//    expert mask through distributed shared memory and builds the union:
+//    ascending unique-expert list, per-expert token ranks, shared blocks on
+//    top.  No global atomics or fences, no second kernel.
+// This is the real counterpart of the reference's stand-ins draw_expert_set
+// / sample_active_experts (expert_model.hpp:100-139): union = distinct
+// routed experts, shared blocks always active on top.
+__global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    float* xs = reinterpret_cast<float*>(rsm);                         // [d] MoE input (bf16 values)
+    const uint16_t* wsm = reinterpret_cast<const uint16_t*>(rsm + (size_t)p.d * 4);  // staged router rows
     __shared__ float red[32];
-    __shared__ float wred[kRouteWarps][kMaxExperts + 1];
-    __shared__ int s_last;
-    __shared__ float s_logits[kMaxT][kMaxExperts + 1];
+    __shared__ float s_lg[kMaxExperts + 1];
+    __shared__ int s_mytopk[kMaxTopK];
+    __shared__ unsigned long long s_mymask[2];
+    __shared__ int s_topk[kMaxT * kMaxTopK];
     __shared__ unsigned long long masks[kMaxT][2];
-    const int slice = blockIdx.x, t = blockIdx.y;
-    const int n_slices = gridDim.x;
+    __shared__ int s_warp_on[kMaxExperts / 32];
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int t = blockIdx.x;
     const int n_rows = p.E + (p.shared_gate ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = slice * kRouteSlice + threadIdx.x;
-    // ---- independent of the predecessor: router + norm weights of the slice
-    for (int e = 0; e < n_rows; ++e) wsl[e * kRouteSlice + threadIdx.x] = p.router_w[(long long)e * p.d + c];
-    const float nw = bits_to_f32(p.norm_w[c]);
+    const bool staged = p.stage_w != 0;
+    // ---- independent of the predecessor
+    if (staged) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.router_w);
+        uint4* dst = reinterpret_cast<uint4*>(rsm + (size_t)p.d * 4);
+        for (int i = threadIdx.x; i < n_rows * p.d / 8; i += kRowThreads) dst[i] = __ldg(src + i);
+    }
     griddep_wait();
     griddep_launch();
     trace_start(p.trace);
-    if (slice == 0 && t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
-    // ---- 1/rms of the full row (every load issued before the reduction)
+    if (t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    // ---- norm
     const float* x = p.x + (long long)t * p.d;
     const float4* x4 = reinterpret_cast<const float4*>(x);
-    float ss = 0.f;
-    for (int i = threadIdx.x; i < (p.d >> 2); i += kRouteThreads) {
-        const float4 v = x4[i];
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    constexpr int kV = 4;  // float4 per thread, d <= 8192
+    float4 xv[kV];
+#pragma unroll
+    for (int j = 0; j < kV; ++j) {
+        const int i = threadIdx.x + j * kRowThreads;
+        xv[j] = i < (p.d >> 2) ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < kV; ++j) ss += xv[j].x * xv[j].x + xv[j].y * xv[j].y + xv[j].z * xv[j].z + xv[j].w * xv[j].w;
     ss = block_sum(ss, red);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
-    const uint16_t b = bf16_bits((x[c] * rinv) * nw);
-    p.xn_bfrag[bfrag_index(t, c)] = b;
-    if (p.tap_xn) p.tap_xn[(long long)t * p.d + c] = b;
-    const float xv = bits_to_f32(b);
-    // ---- partial router logits of the slice (fixed reduction order)
-    for (int e = 0; e < n_rows; ++e) {
-        float v = xv * bits_to_f32(wsl[e * kRouteSlice + threadIdx.x]);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) wred[warp][e] = v;
+    for (int j = 0; j < kV; ++j) {
+        const int i = threadIdx.x + j * kRowThreads;
+        if (i >= (p.d >> 2)) continue;
+        const float vv[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = 4 * i + q;
+            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[c]));
+            p.xn_bfrag[bfrag_index(t, c)] = b;
+            if (p.tap_xn) p.tap_xn[(long long)t * p.d + c] = b;
+            xs[c] = bits_to_f32(b);
+        }
     }
     if (p.zero_nonlocal) {
         // EP: every (token, rank) row is written by exactly one rank's down
         // GEMV; the others must contribute exact zeros to the all-reduce.
-        float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d;
-        for (int r = 0; r < p.k + p.S; ++r) y[(long long)r * p.d + c] = 0.f;
+        float4* y = reinterpret_cast<float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
+        for (int i = threadIdx.x; i < (p.k + p.S) * p.d / 4; i += kRowThreads) y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
-    if (threadIdx.x < n_rows) {
-        float v = 0.f;
-        for (int w = 0; w < kRouteWarps; ++w) v += wred[w][threadIdx.x];
-        p.logit_part[((long long)t * n_slices + slice) * (p.E + 1) + threadIdx.x] = v;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.ticket, 1) == (int)(gridDim.x * gridDim.y) - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-
-    // ---- routing of all tokens (last CTA)
-    for (int q = threadIdx.x; q < p.T * n_rows; q += kRouteThreads) {
-        const int tt = q / n_rows, e = q - tt * n_rows;
-        float pv[kMaxSlices];
-#pragma unroll
-        for (int sl = 0; sl < kMaxSlices; ++sl)
-            pv[sl] = sl < n_slices ? __ldcg(p.logit_part + ((long long)tt * n_slices + sl) * (p.E + 1) + e) : 0.f;
-        float v = 0.f;
-#pragma unroll
-        for (int sl = 0; sl < kMaxSlices; ++sl)
-            if (sl < n_slices) v += pv[sl];
-        s_logits[tt][e] = v;
-        p.logits[tt * (p.E + 1) + e] = v;
+    // ---- router logits: warp per expert row, lane-strided 8-element pieces
+    for (int e = warp; e < n_rows; e += kRowWarps) {
+        const uint4* w4 = staged ? reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d)
+                                 : reinterpret_cast<const uint4*>(p.router_w + (size_t)e * p.d);
+        float acc = 0.f;
+        for (int i = lane; i < p.d / 8; i += 32) {
+            const uint4 w = staged ? w4[i] : __ldg(w4 + i);
+            const float4 a = reinterpret_cast<const float4*>(xs)[2 * i];
+            const float4 b = reinterpret_cast<const float4*>(xs)[2 * i + 1];
+            acc = fmaf(a.x, __uint_as_float(w.x << 16), acc);
+            acc = fmaf(a.y, __uint_as_float(w.x & 0xFFFF0000u), acc);
+            acc = fmaf(a.z, __uint_as_float(w.y << 16), acc);
+            acc = fmaf(a.w, __uint_as_float(w.y & 0xFFFF0000u), acc);
+            acc = fmaf(b.x, __uint_as_float(w.z << 16), acc);
+            acc = fmaf(b.y, __uint_as_float(w.z & 0xFFFF0000u), acc);
+            acc = fmaf(b.z, __uint_as_float(w.w << 16), acc);
+            acc = fmaf(b.w, __uint_as_float(w.w & 0xFFFF0000u), acc);
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            s_lg[e] = acc;
+            p.logits[t * (p.E + 1) + e] = acc;
+        }
     }
     __syncthreads();
-    __shared__ int s_topk[kMaxT * kMaxTopK];
-    __shared__ int s_warp_on[kMaxExperts / 32];
-    for (int tt = warp; tt < p.T; tt += kRouteWarps) {
-        const float* lg = s_logits[tt];
+    // ---- softmax + top-k of this token (warp 0)
+    if (warp == 0) {
+        const int tt = t;
+        const float* lg = s_lg;
         float v[kMaxExperts / 32];
         float m = -INFINITY;
 #pragma unroll
@@ -215,18 +239,33 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
         }
         const float den = p.renorm ? zk : z;
         if (lane < p.k) {
-            s_topk[tt * p.k + lane] = my_i;
+            s_mytopk[lane] = my_i;
             p.topk_id[tt * p.k + lane] = my_i;
             p.topk_w[tt * p.k + lane] = my_e / den;
         }
         if (lane == 0) {
             p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-lg[p.E])) : 1.0f;
-            masks[tt][0] = m0;
-            masks[tt][1] = m1;
+            s_mymask[0] = m0;
+            s_mymask[1] = m1;
         }
     }
+    cluster.sync();  // every token's top-k and mask visible cluster-wide
+    if (cluster.block_rank() != 0) {
+        cluster.sync();  // keep this CTA's shared memory alive until rank 0 has read it
+        return;
+    }
+    // ---- expert union (rank 0): gather through distributed shared memory
+    for (int q = threadIdx.x; q < p.T * p.k; q += kRowThreads) {
+        const int tt = q / p.k, r = q - tt * p.k;
+        s_topk[q] = cluster.map_shared_rank(s_mytopk, tt)[r];
+    }
+    if (threadIdx.x < 2 * p.T) {
+        const int tt = threadIdx.x >> 1, h = threadIdx.x & 1;
+        masks[tt][h] = cluster.map_shared_rank(s_mymask, tt)[h];
+    }
     __syncthreads();
-    // expert union: thread e owns expert e; ballots give ascending slots
+    cluster.sync();  // peers may exit now
+    // thread e owns expert e; ballots give ascending slots
     unsigned long long u0 = 0, u1 = 0;
     for (int tt = 0; tt < p.T; ++tt) {
         u0 |= masks[tt][0];
@@ -265,7 +304,6 @@ __global__ void __launch_bounds__(kRouteThreads) moe_route_kernel(RouteParams p)
             ++lb;
         }
         *p.count = n;
-        *p.ticket = 0;
     }
 }
 
@@ -289,83 +327,83 @@ struct CombineParams {
     unsigned long long* trace;
 };
 
-// grid = (d / kRouteSlice, T).  CTA (slice, t): residual += sum_r w[t][r] *
-// Y[t][r] (+ shared-gate * sum_b Y[t][k+b]) for its columns in fixed order,
-// one column per thread with every load independent; the slice's sum of
-// squares goes to ss_part.  The last slice CTA of token t (per-token ticket)
-// sums the partials in slice order and writes the next RMSNorm (next
-// layer's attention input, or the final norm) for the whole row.
-__global__ void __launch_bounds__(kRouteThreads) moe_combine_kernel(CombineParams p) {
+// grid = T CTAs of 1024 threads, one token row each, a single pass with
+// every load issued up front: residual += sum_r w[t][r] * Y[t][r]
+// (+ shared-gate * sum_b Y[t][k+b]) in fixed order, then the next RMSNorm
+// (next layer's attention input, or the final norm) of the updated row.
+__global__ void __launch_bounds__(kRowThreads) moe_combine_kernel(CombineParams p) {
     __shared__ float red[32];
-    __shared__ int s_last;
-    const int slice = blockIdx.x, t = blockIdx.y;
-    const int n_slices = gridDim.x;
-    const int c = slice * kRouteSlice + threadIdx.x;
+    const int t = blockIdx.x;
     griddep_wait();
     griddep_launch();
     trace_start(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
-    const float* y = p.ycontrib + (long long)t * (p.k + p.S) * p.d + c;
-    float* xr = p.x + (long long)t * p.d;
-    // all loads first (one round trip), then the fixed-order sums
-    float yv[kMaxTopK], wr[kMaxTopK], ys[kMaxTopK];
+    constexpr int kV = 4;  // float4 per thread, d <= 8192
+    const int n4 = p.d >> 2;
+    const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
+    float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
+    const float g = __ldg(p.gsh + t);
+    float4 nx[kV];
+    float ss = 0.f;
 #pragma unroll
-    for (int r = 0; r < kMaxTopK; ++r) {
-        if (r < p.k) {
-            yv[r] = y[(long long)r * p.d];
-            wr[r] = __ldg(p.topk_w + t * p.k + r);
+    for (int j = 0; j < kV; ++j) {
+        const int i = threadIdx.x + j * kRowThreads;
+        if (i >= n4) {
+            nx[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
         }
-        if (r < p.S) ys[r] = y[(long long)(p.k + r) * p.d];
+        const float4 x0 = x4[i];
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int nr = p.k + p.S;
+        for (int r0 = 0; r0 < nr; r0 += 4) {  // loads in batches of 4 rows, sums in row order
+            float4 yb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (r0 + q < nr) yb[q] = y4[(long long)(r0 + q) * n4 + i];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = r0 + q;
+                if (r < p.k) {
+                    const float w = __ldg(p.topk_w + t * p.k + r);
+                    acc.x += w * yb[q].x;
+                    acc.y += w * yb[q].y;
+                    acc.z += w * yb[q].z;
+                    acc.w += w * yb[q].w;
+                } else if (r < nr) {
+                    sh.x += yb[q].x;
+                    sh.y += yb[q].y;
+                    sh.z += yb[q].z;
+                    sh.w += yb[q].w;
+                }
+            }
+        }
+        if (p.S > 0) {
+            acc.x += g * sh.x;
+            acc.y += g * sh.y;
+            acc.z += g * sh.z;
+            acc.w += g * sh.w;
+        }
+        if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
+        nx[j] = make_float4(x0.x + acc.x, x0.y + acc.y, x0.z + acc.z, x0.w + acc.w);
+        x4[i] = nx[j];
+        if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = nx[j];
+        ss += nx[j].x * nx[j].x + nx[j].y * nx[j].y + nx[j].z * nx[j].z + nx[j].w * nx[j].w;
     }
-    const float x0 = xr[c];
-    float acc = 0.f;
+    ss = block_sum(ss, red);
+    const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
 #pragma unroll
-    for (int r = 0; r < kMaxTopK; ++r)
-        if (r < p.k) acc += wr[r] * yv[r];
-    if (p.S > 0) {
-        float sh = 0.f;
+    for (int j = 0; j < kV; ++j) {
+        const int i = threadIdx.x + j * kRowThreads;
+        if (i >= n4) continue;
+        const float vv[4] = {nx[j].x, nx[j].y, nx[j].z, nx[j].w};
 #pragma unroll
-        for (int b = 0; b < kMaxTopK; ++b)
-            if (b < p.S) sh += ys[b];
-        acc += __ldg(p.gsh + t) * sh;
-    }
-    if (p.tap_moe) p.tap_moe[(long long)t * p.d + c] = acc;
-    const float nx = x0 + acc;
-    xr[c] = nx;
-    if (p.tap_x) p.tap_x[(long long)t * p.d + c] = nx;
-    const float ss = block_sum(nx * nx, red);
-    if (threadIdx.x == 0) p.ss_part[t * n_slices + slice] = ss;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.tok_ticket + t, 1) == n_slices - 1);
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // every load of the tail issued before any use (one L2 round trip each)
-    float xv[kMaxSlices], wv[kMaxSlices], sp[kMaxSlices];
-#pragma unroll
-    for (int j = 0; j < kMaxSlices; ++j) {
-        if (j < n_slices) {
-            xv[j] = __ldcg(xr + j * kRouteSlice + threadIdx.x);
-            wv[j] = bits_to_f32(p.norm_w[j * kRouteSlice + threadIdx.x]);
-            sp[j] = __ldcg(p.ss_part + t * n_slices + j);
+        for (int q = 0; q < 4; ++q) {
+            const int col = 4 * i + q;
+            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[col]));
+            p.xn_bfrag[p.umma ? umma_b_index(t, col) : bfrag_index(t, col)] = b;
+            if (p.tap_xn) p.tap_xn[(long long)t * p.d + col] = b;
         }
     }
-    float tot = 0.f;
-#pragma unroll
-    for (int j = 0; j < kMaxSlices; ++j)
-        if (j < n_slices) tot += sp[j];
-    const float rinv = 1.0f / sqrtf(tot / (float)p.d + p.eps);
-#pragma unroll
-    for (int j = 0; j < kMaxSlices; ++j) {
-        if (j < n_slices) {
-            const int i = j * kRouteSlice + threadIdx.x;
-            const uint16_t b = bf16_bits((xv[j] * rinv) * wv[j]);
-            p.xn_bfrag[p.umma ? umma_b_index(t, i) : bfrag_index(t, i)] = b;
-            if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
-        }
-    }
-    if (threadIdx.x == 0) p.tok_ticket[t] = 0;
 }
 
 // Step entry: token embedding + first RMSNorm + the step's RoPE table;
