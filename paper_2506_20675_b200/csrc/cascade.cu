@@ -151,7 +151,7 @@ struct Dims {
     }
 };
 
-static int g_route_stage = 0;  // CASCADE_ROUTE_STAGE=1: stage router weights in smem (A/B: off measured faster)
+static int g_route_stage = 1;  // CASCADE_ROUTE_STAGE=0: read router rows from global (A/B: staging measured faster)
 static bool route_staged(const Dims& D, int shared_gate) {
     return g_route_stage && (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2 <= (size_t)kRouteStageBytes;
 }

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         const uint4* w4 = staged ? reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d)
                                  : reinterpret_cast<const uint4*>(p.router_w + (size_t)e * p.d);
         float acc = 0.f;
+#pragma unroll 8
         for (int i = lane; i < p.d / 8; i += 32) {
             const uint4 w = staged ? w4[i] : __ldg(w4 + i);
             const float4 a = reinterpret_cast<const float4*>(xs)[2 * i];

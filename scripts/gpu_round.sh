@@ -1,4 +1,4 @@
-# One GPU pass: parity tests, smoke, bench (both arms), ncu launch list + full capture of the expert GEMVs.
+# One GPU pass: parity tests, smoke, bench (both arms), ncu launch list + full capture of the GEMVs.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
@@ -7,14 +7,20 @@ timeout 1500 python -m pytest tests -m gpu -q -rA > gpurun_out/pytest_gpu_$TAG.t
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.txt 2>&1
 echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.txt
-timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
 timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 echo "bench rc=$?" >> gpurun_out/bench_$TAG.err
+if [ -n "$ARM_B" ]; then
+env $ARM_B timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_${TAG}_b.json 2> gpurun_out/bench_${TAG}_b.err
+fi
 if [ -z "$SKIP_NCU" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file gpurun_out/launches_$TAG.csv python scripts/profile_step.py --ks 0,8 > gpurun_out/prof_launch_$TAG.log 2>&1
 echo "ncu1 rc=$?" >> gpurun_out/prof_launch_$TAG.log
 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:stream_gemv_kernel -c 8 -o gpurun_out/gemv_full_$TAG python scripts/profile_step.py --ks 8 --layers 2 > gpurun_out/prof_full_$TAG.log 2>&1
+  -k regex:stream_gemv -c 8 -o gpurun_out/gemv_full_$TAG python scripts/profile_step.py --ks 8 --layers 2 > gpurun_out/prof_full_$TAG.log 2>&1
 echo "ncu2 rc=$?" >> gpurun_out/prof_full_$TAG.log
+timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
+  -k regex:"moe_route|moe_combine|attn_partial|attn_combine" -c 8 -o gpurun_out/small_full_$TAG python scripts/profile_step.py --ks 0 --layers 2 > gpurun_out/prof_small_$TAG.log 2>&1
+echo "ncu3 rc=$?" >> gpurun_out/prof_small_$TAG.log
 fi
