@@ -194,6 +194,14 @@ CASCADE_API int cascade_profile_step(cascade_session* s, int K, double* ns, int3
  * cascade_profile_step. */
 CASCADE_API int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n);
 
+/* Per-CTA timeline of one captured step of width K+1 (diagnostic, commit =
+ * 0): out[(i * 512 + cta) * 2 + {0, 1}] = %globaltimer (ns) when CTA `cta`
+ * of launch i started (after its dependency wait) and when it exited; 0
+ * for CTAs that do not exist (cta >= 512 is not recorded).  kind[i] as in
+ * cascade_profile_step; *n_slots = launches (<= cap_slots). */
+CASCADE_API int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, int32_t* kind, int cap_slots,
+                                       int* n_slots);
+
 /* Number of kernel launches one step of width K+1 performs (graph nodes
  * that are kernels). */
 CASCADE_API int cascade_step_kernel_count(cascade_session* s, int K, int* out);

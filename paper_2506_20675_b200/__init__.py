@@ -229,6 +229,11 @@ def lib() -> ctypes.CDLL:
             ctypes.c_int,
             [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
         ),
+        "cascade_step_cta_trace": (
+            ctypes.c_int,
+            [P, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(i32), ctypes.c_int,
+             ctypes.POINTER(ctypes.c_int)],
+        ),
         "cascade_profile_step": (
             ctypes.c_int,
             [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
@@ -425,6 +430,17 @@ class Session:
         _check(lib().cascade_step_trace(self.h, K, ns.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), _i32p(kind),
                                         cap, ctypes.byref(n)))
         return ns[: n.value], kind[: n.value]
+
+    def cta_trace(self, K: int):
+        """Per-CTA (start, exit) globaltimer stamps of one captured step:
+        array [launches][512][2] (ns, 0 = no such CTA) and the launch classes."""
+        cap = 64 * self.model.shape.num_layers + 16
+        out = np.zeros((cap, 512, 2), np.uint64)
+        kind = np.zeros(cap, np.int32)
+        n = ctypes.c_int()
+        _check(lib().cascade_step_cta_trace(self.h, K, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                            _i32p(kind), cap, ctypes.byref(n)))
+        return out[: n.value], kind[: n.value]
 
     def enable_taps(self, on: bool = True):
         _check(lib().cascade_enable_taps(self.h, 1 if on else 0))

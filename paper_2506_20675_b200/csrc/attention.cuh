@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         kv_pending = true;
     }
     griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
+    griddep_launch_early();
+    CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     const int nch = (ctx + kChunk - 1) / kChunk;
     const int n_items = (nch + 1) * p.KV;
@@ -328,8 +328,8 @@ constexpr int kMaxChunksSmem = 1024;
 
 __global__ void attn_combine_kernel(AttnCombineParams p) {
     griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
+    griddep_launch_early();
+    CTA_TRACE(p.trace);
     __shared__ float scale_c[kMaxChunksSmem];
     __shared__ float red[32];
     const int t = blockIdx.x, h = blockIdx.y;

@@ -411,7 +411,7 @@ struct AcceptParams {
 
 __global__ void accept_kernel(AcceptParams p) {
     griddep_wait();
-    trace_start(p.trace);
+    CTA_TRACE(p.trace);
     if (threadIdx.x != 0) return;
     const uint64_t t_end = globaltimer();
     if (p.trace) p.trace[1] = t_end;
@@ -570,6 +570,7 @@ struct cascade_session {
     int l2_prologue = 0;  // measured slower (down-proj ranges exceed L2; QKV prefetch slows the combine)
     int gemv_trigger = 0;  // early launch_dependents from the GEMVs measured slower (A/B in profiles/r01)
     int down_early = 1;
+    int umma_prologue = 1;
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -688,6 +689,11 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = v[0] == '1';
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
+    if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
+    if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
+        const int late = v[0] == '1';
+        cudaMemcpyToSymbol(g_late_trigger, &late, sizeof(late));
+    }
     // attention smem opt-in
     const int asmem = D.hd == 32 ? attn_smem_bytes<32>() : D.hd == 64 ? attn_smem_bytes<64>() : attn_smem_bytes<128>();
     if (D.hd == 32) e = cudaFuncSetAttribute(attn_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
@@ -791,6 +797,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.n_blocks = 1;
     p.partial = s->upartial;
     p.counters = s->ucounters;
+    p.no_prologue = !s->umma_prologue;
     return p;
 }
 
@@ -1215,6 +1222,40 @@ extern "C" int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t
         kind[i] = s->trace_kind[T][i];
     }
     *n = cnt;
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, int32_t* kind, int cap_slots,
+                                      int* n_slots) {
+    if (!s || !out || !kind || !n_slots || K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "bad arguments");
+    if (s->taps_on) return set_err(CASCADE_EINVAL, "CTA trace needs the captured path (disable taps)");
+    CK(cudaSetDevice(s->m->device));
+    const int T = K + 1;
+    int rc = ensure_graph(s, T);
+    if (rc) return rc;
+    const int cnt = s->trace_n[T];
+    if (cnt > cap_slots) return set_err(CASCADE_EINVAL, "trace buffer too small: need " + std::to_string(cnt));
+    const size_t bytes = (size_t)cnt * kCtaTraceCap * 2 * 8;
+    unsigned long long* buf = nullptr;
+    CK(cudaMalloc(&buf, bytes));
+    CK(cudaMemset(buf, 0, bytes));
+    unsigned long long* base = s->trace;
+    CK(cudaMemcpyToSymbol(g_cta_trace_base, &base, sizeof(base)));
+    CK(cudaMemcpyToSymbol(g_cta_trace, &buf, sizeof(buf)));
+    s->h_params->mode = 0;
+    s->h_params->commit = 0;
+    s->h_params->T = T;
+    s->h_params->t_base_ns = s->t_base_ns;
+    rc = run_step(s, T);
+    cudaError_t e = cudaStreamSynchronize(s->stream);
+    unsigned long long* null = nullptr;
+    cudaMemcpyToSymbol(g_cta_trace, &null, sizeof(null));
+    if (rc == CASCADE_OK && e == cudaSuccess) e = cudaMemcpy(out, buf, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (rc) return rc;
+    if (e != cudaSuccess) return set_err(CASCADE_ECUDA, cudaGetErrorString(e));
+    for (int i = 0; i < cnt; ++i) kind[i] = s->trace_kind[T][i];
+    *n_slots = cnt;
     return CASCADE_OK;
 }
 

@@ -41,6 +41,13 @@ __device__ __forceinline__ uint64_t globaltimer_raw() {
 // rasterisation overlap the predecessor's tail.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// A/B switch (CASCADE_LATE_TRIGGER=1): latency-bound kernels let their
+// dependents launch only at exit, so the next GEMV's weight prologue does
+// not compete with their loads.
+__device__ int g_late_trigger = 0;
+__device__ __forceinline__ void griddep_launch_early() {
+    if (!g_late_trigger) griddep_launch();
+}
 
 // Bulk L2 prefetch of an upcoming weight matrix, spread over every thread
 // of the grid.  Issued from latency-bound kernels (attention, combine) so
@@ -63,10 +70,50 @@ __device__ __forceinline__ void prefetch_l2(const void* base, unsigned long long
     }
 }
 
+// Per-CTA timeline (diagnostic, cascade_step_cta_trace): when g_cta_trace
+// is set, every CTA records the globaltimer at its start (after
+// griddepcontrol.wait) and at its exit, at [(slot * kCtaTraceCap + cta) * 2].
+// Null in normal runs: one predicated global load per kernel.
+constexpr int kCtaTraceCap = 512;
+constexpr int kPhaseBase = 496;  // CTA records >= this hold CTA 0's phase stamps
+__device__ unsigned long long* g_cta_trace = nullptr;
+__device__ unsigned long long* g_cta_trace_base = nullptr;  // the session's trace slot 0
+
+__device__ __forceinline__ unsigned long long* cta_trace_slot(unsigned long long* slot) {
+    unsigned long long* buf = g_cta_trace;
+    if (buf == nullptr || slot == nullptr) return nullptr;
+    const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+    if (cta >= kPhaseBase) return nullptr;
+    return buf + ((slot - g_cta_trace_base) * kCtaTraceCap + cta) * 2;
+}
+
 // per-kernel start stamp for in-graph tracing (block 0, thread 0)
 __device__ __forceinline__ void trace_start(unsigned long long* slot) {
     if (slot != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *slot = globaltimer_raw();
+    if (threadIdx.x == 0) {
+        unsigned long long* c = cta_trace_slot(slot);
+        if (c != nullptr) c[0] = globaltimer_raw();
+    }
 }
+
+// CTA exit stamp: the latest warp to leave wins (RAII: every return path).
+struct CtaExitStamp {
+    unsigned long long* c;
+    __device__ explicit CtaExitStamp(unsigned long long* slot) : c(cta_trace_slot(slot)) {}
+    __device__ ~CtaExitStamp() {
+        if (c != nullptr && (threadIdx.x & 31) == 0) atomicMax(c + 1, globaltimer_raw());
+    }
+};
+// Phase stamps of CTA 0 (diagnostic): stamp i of a launch goes to the
+// unused CTA records 496.. of its slot (scripts/cta_timeline.py).
+__device__ __forceinline__ void phase_stamp(unsigned long long* slot, int i) {
+    unsigned long long* buf = g_cta_trace;
+    if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
+    buf[(slot - g_cta_trace_base) * kCtaTraceCap * 2 + kPhaseBase * 2 + i] = globaltimer_raw();
+}
+#define CTA_TRACE(slot)   \
+    trace_start(slot);    \
+    CtaExitStamp cta_exit_stamp_(slot)
 
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;

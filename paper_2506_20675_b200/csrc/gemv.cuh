@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     }
     griddep_wait();
     if (p.trigger) griddep_launch();
-    trace_start(p.trace);
+    CTA_TRACE(p.trace);
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
     const int U = p.count ? *p.count : p.n_blocks;
     const long long per_block = (long long)p.n_st * p.n_ks;

@@ -115,6 +115,7 @@ struct UGemvParams {
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
     unsigned long long* trace; // in-graph trace slot
     unsigned long long* dbg;   // optional phase stamps (scripts/umma_probe.cu)
+    int no_prologue;           // A/B: issue nothing before griddepcontrol.wait
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
                     ++i;
                 }
             };
-            if (early && lane == 0) issue(kUStages, false);  // PDL prologue: weights overlap the predecessor's tail
+            if (early && lane == 0 && !p.no_prologue) issue(kUStages, false);  // PDL prologue: weights overlap the predecessor's tail
             griddep_wait();
             griddep_launch();
             if (lane != 0) goto producer_done;
@@ -498,6 +499,10 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0 && p.dbg) atomicMax(p.dbg + 9, globaltimer_raw());
+    if (threadIdx.x == 0) {
+        unsigned long long* c = cta_trace_slot(p.trace);
+        if (c != nullptr) c[1] = globaltimer_raw();
+    }
     if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");

@@ -120,9 +120,10 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         for (int i = threadIdx.x; i < n_rows * p.d / 8; i += kRowThreads) dst[i] = __ldg(src + i);
     }
     griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
+    griddep_launch_early();
+    CTA_TRACE(p.trace);
     if (t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    phase_stamp(p.trace, 0);
     // ---- norm
     const float* x = p.x + (long long)t * p.d;
     const float4* x4 = reinterpret_cast<const float4*>(x);
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         for (int i = threadIdx.x; i < (p.k + p.S) * p.d / 4; i += kRowThreads) y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
+    phase_stamp(p.trace, 1);
     // ---- router logits: warp per expert row, lane-strided 8-element pieces
     for (int e = warp; e < n_rows; e += kRowWarps) {
         const uint4* w4 = staged ? reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d)
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         }
     }
     __syncthreads();
+    phase_stamp(p.trace, 2);
     // ---- softmax + top-k of this token (warp 0)
     if (warp == 0) {
         const int tt = t;
@@ -250,7 +253,9 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
             s_mymask[1] = m1;
         }
     }
+    phase_stamp(p.trace, 3);
     cluster.sync();  // every token's top-k and mask visible cluster-wide
+    phase_stamp(p.trace, 4);
     if (cluster.block_rank() != 0) {
         cluster.sync();  // keep this CTA's shared memory alive until rank 0 has read it
         return;
@@ -266,6 +271,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
     }
     __syncthreads();
     cluster.sync();  // peers may exit now
+    phase_stamp(p.trace, 5);
     // thread e owns expert e; ballots give ascending slots
     unsigned long long u0 = 0, u1 = 0;
     for (int tt = 0; tt < p.T; ++tt) {
@@ -306,6 +312,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         }
         *p.count = n;
     }
+    phase_stamp(p.trace, 6);
 }
 
 struct CombineParams {
@@ -336,9 +343,10 @@ __global__ void __launch_bounds__(kRowThreads) moe_combine_kernel(CombineParams 
     __shared__ float red[32];
     const int t = blockIdx.x;
     griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
+    griddep_launch_early();
+    CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
+    phase_stamp(p.trace, 0);
     constexpr int kV = 4;  // float4 per thread, d <= 8192
     const int n4 = p.d >> 2;
     const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
@@ -390,7 +398,9 @@ __global__ void __launch_bounds__(kRowThreads) moe_combine_kernel(CombineParams 
         if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = nx[j];
         ss += nx[j].x * nx[j].x + nx[j].y * nx[j].y + nx[j].z * nx[j].z + nx[j].w * nx[j].w;
     }
+    phase_stamp(p.trace, 1);
     ss = block_sum(ss, red);
+    phase_stamp(p.trace, 2);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
 #pragma unroll
     for (int j = 0; j < kV; ++j) {
@@ -405,6 +415,7 @@ __global__ void __launch_bounds__(kRowThreads) moe_combine_kernel(CombineParams 
             if (p.tap_xn) p.tap_xn[(long long)t * p.d + col] = b;
         }
     }
+    phase_stamp(p.trace, 3);
 }
 
 // Step entry: token embedding + first RMSNorm + the step's RoPE table;
@@ -449,8 +460,8 @@ struct EmbedParams {
 
 __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p) {
     griddep_wait();
-    griddep_launch();
-    trace_start(p.trace);
+    griddep_launch_early();
+    CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     __shared__ float red[32];
     const int t = blockIdx.x;

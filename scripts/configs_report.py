@@ -17,6 +17,7 @@ import sys
 import time
 
 import numpy as np
+import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -47,11 +48,14 @@ def latency_sweep(shape, ctx=1024, reps=5, prompts=4, seed=1):
         for K in KS:
             ns, kind = s.trace(K)  # one captured step; union sizes of this step
             u_acc[K].append(float(np.mean(s.union_sizes())))
-            t0 = time.perf_counter()
+            st = torch.cuda.ExternalStream(s.stream(), device="cuda:0")
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
             for _ in range(reps):
-                s.enqueue(K)
+                s.enqueue(K, commit=False)
+            e1.record(st)
             s.sync()
-            lat[K].append((time.perf_counter() - t0) / reps * 1e6)
+            lat[K].append(e0.elapsed_time(e1) / reps * 1e3)  # device time on the session stream
         s.close()
     for K in KS:
         U = float(np.mean(u_acc[K]))
