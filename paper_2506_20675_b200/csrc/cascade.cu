@@ -568,7 +568,7 @@ struct cascade_session {
     int trace_n[kMaxT + 1] = {};
     bool prefetch = true;
     int l2_prologue = 0;  // measured slower (down-proj ranges exceed L2; QKV prefetch slows the combine)
-    int gemv_trigger = 0;  // early launch_dependents from the GEMVs measured slower (A/B in profiles/r01)
+    int gemv_trigger = 1;  // early launch_dependents: the down GEMV builds its union and requests its first weights while gate/up drains
     int down_early = 1;
     int umma_prologue = 1;
     uint16_t* kc = nullptr;
@@ -701,7 +701,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     if (e == cudaSuccess) e = set_carveouts(D.hd);
     if (const char* v = getenv("CASCADE_ROUTE_STAGE")) g_route_stage = atoi(v);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    (void)0;
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)route_smem_bytes(D, m->g.shared_gate));
@@ -762,23 +762,18 @@ static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStrea
 
 
 
-// moe_route_kernel: one thread-block cluster of T CTAs (T <= 16, the
-// non-portable cluster size is opted into at session creation), PDL.
+// moe_route_kernel: T independent CTAs (one per token), PDL.
 static cudaError_t launch_route(const RouteParams& p, int T, size_t smem, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(T);
     cfg.blockDim = dim3(kRowThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = T;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 2;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, moe_route_kernel, p);
 }
 
@@ -984,15 +979,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.router_w = w.router;
         rp.xn_bfrag = s->xn;
         rp.logits = s->logits_router;
-        rp.logit_part = s->logit_part;
-        rp.ticket = s->ticket;
         rp.topk_id = s->topk_id;
         rp.topk_w = s->topk_w;
         rp.gsh = s->gsh;
-        rp.list = s->list;
-        rp.count = s->count;
-        rp.route_rank = s->route_rank;
-        rp.union_size = s->union_size + l;
         rp.ycontrib = s->ycontrib;
         rp.tap_xn = taps ? s->taps.xn_moe + td : nullptr;
         rp.T = T;
@@ -1015,6 +1004,11 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         CK(launch_route(rp, T, route_smem_bytes(D, m->g.shared_gate), st));
         PE();
         ++nk;
+        if (getenv("CASCADE_ROUTE_TWICE")) {  // i-cache experiment
+            rp.trace = tr(5);
+            CK(launch_route(rp, T, route_smem_bytes(D, m->g.shared_gate), st));
+            ++nk;
+        }
         if (taps) {
             CK(cudaMemcpyAsync(s->taps.logits + (size_t)l * kMaxT * (D.E + 1), s->logits_router,
                                (size_t)T * (D.E + 1) * 4, cudaMemcpyDeviceToDevice, st));
@@ -1024,13 +1018,27 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
                                cudaMemcpyDeviceToDevice, st));
         }
         // experts: gate/up (+SiLU) then down, over the active list only
+        auto set_union = [&](GemvParams& q) {
+            q.topk_id = s->topk_id;
+            q.k_top = D.k;
+            q.E = D.E;
+            q.e_lo = m->e_lo;
+            q.e_hi = m->e_hi;
+            q.S = D.S;
+            q.ep_rank = m->ep_rank;
+            q.ep_size = m->ep_size;
+        };
         GemvParams gu = gemv_base(s, T);
         gu.W = w.w13;
         gu.w_block_stride = D.w13_vec;
         gu.B = reinterpret_cast<const uint2*>(s->xn);
         gu.b_block_stride = 0;
-        gu.list = s->list;
+        gu.list = s->list;    // published union (CTA 0): accept, telemetry, taps
         gu.count = s->count;
+        gu.route_rank = s->route_rank;
+        gu.union_size = s->union_size + l;
+        gu.publish = 1;
+        set_union(gu);
         gu.n_st = 2 * D.f / kSTRows;
         gu.n_ks = D.d / 16;
         gu.hout = s->hbuf;
@@ -1045,12 +1053,10 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         dn.w_block_stride = D.w2_vec;
         dn.B = reinterpret_cast<const uint2*>(s->hbuf);
         dn.b_block_stride = (long long)D.f * 4;  // uint2 units per slot
-        dn.list = s->list;
-        dn.count = s->count;
+        set_union(dn);
         dn.n_st = D.d / kSTRows;
         dn.n_ks = D.f / 16;
-        dn.route_rank = s->route_rank;
-        dn.early_list = s->down_early && s->gemv_trigger;  // list/count from moe_route, two kernels back
+        dn.early_list = s->down_early;  // union from the router's top-k, written two kernels back
         dn.n_contrib = D.k + D.S;
         dn.out = s->ycontrib;
         dn.ld = D.d;

@@ -40,8 +40,8 @@ struct GemvParams {
     long long w_block_stride;  // uint4 units between blocks
     const uint2* B;            // B-frag activations (list slot 0)
     long long b_block_stride;  // uint2 units between list slots (0: shared X)
-    const int* list;           // active block ids, or nullptr (identity)
-    const int* count;          // device U, or nullptr (use n_blocks)
+    int* list;                 // active block ids, or nullptr (identity)
+    int* count;                // device U, or nullptr (use n_blocks)
     int n_blocks;
     int n_st;                  // super-tiles per block
     int n_ks;                  // k-steps per block (K / 16)
@@ -53,7 +53,7 @@ struct GemvParams {
     int ld;                    // leading dimension of out
     uint16_t* hout;            // EPI_GATEUP output (B-frag bf16)
     long long h_block_stride;  // bf16 units between list slots
-    const int* route_rank;     // EPI_DOWN: [slot][16] -> rank in token's list or -1
+    int* route_rank;           // EPI_DOWN: [slot][16] -> rank in token's list or -1
     int n_contrib;             // EPI_DOWN
     unsigned long long* keys;  // EPI_ARGMAX
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
@@ -61,17 +61,109 @@ struct GemvParams {
     int early_list;            // list/count final before griddepcontrol.wait (expert down projection)
     int l2_prologue;           // also L2-prefetch the rest of each warp's range before the wait
     int trigger;               // griddepcontrol.launch_dependents right after the wait
+    // Routed blocks: when topk_id is set, every CTA builds the expert union
+    // itself from the router's top-k (no separate union kernel, no
+    // cross-CTA synchronisation in the router); list / count / route_rank
+    // above are then outputs, written by CTA 0 when `publish` is set.
+    const int* topk_id;        // [T][k_top] routed expert ids (router output)
+    int k_top, E, e_lo, e_hi;  // routed experts; local ones are [e_lo, e_hi)
+    int S, ep_rank, ep_size;   // shared blocks; shared block b lives on rank b % ep_size
+    int publish;
+    int* union_size;           // out (publish): distinct routed experts of the step
 };
 
 constexpr int kGemvThreads = 256;
 constexpr int kGemvWarps = kGemvThreads / 32;
+constexpr int kUnionExperts = 128;                 // expert_model.hpp:96 (kMaxRoutedExperts)
+constexpr int kMaxSlots = kUnionExperts + 16;      // local routed + shared blocks
+
+struct UnionSmem {
+    int list[kMaxSlots];                 // slot -> local block id (ascending routed, then shared)
+    int slot_of[kUnionExperts];          // routed expert -> slot (local only)
+    signed char rank[kMaxSlots][kMaxT];  // slot, token -> rank in the token's contribution list, or -1
+    int count;                           // active local blocks
+    int union_size;                      // distinct routed experts (global)
+};
+
+// One warp: the expert union of the T tokens' top-k (the real counterpart
+// of the reference's sample_active_experts, expert_model.hpp:120-139:
+// union = distinct routed experts; shared blocks always active on top),
+// as the ascending list of local blocks and per-(slot, token) ranks.
+__device__ __forceinline__ void build_union(const GemvParams& p, UnionSmem& u) {
+    const int lane = threadIdx.x & 31;
+    const int n = p.T * p.k_top;  // <= 16 * 16
+    int ev[8];
+    unsigned long long m0 = 0, m1 = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int i = lane + 32 * j;
+        ev[j] = i < n ? __ldcg(p.topk_id + i) : -1;
+        if (ev[j] >= 0) {
+            if (ev[j] < 64) m0 |= 1ull << ev[j];
+            else m1 |= 1ull << (ev[j] - 64);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 |= __shfl_xor_sync(0xffffffffu, m0, o);
+        m1 |= __shfl_xor_sync(0xffffffffu, m1, o);
+    }
+    int base = 0;
+#pragma unroll
+    for (int q = 0; q < kUnionExperts / 32; ++q) {
+        const int e = 32 * q + lane;
+        const bool in = e < p.E && (((e < 64 ? (m0 >> e) : (m1 >> (e - 64))) & 1ull) != 0);
+        const bool loc = in && e >= p.e_lo && e < p.e_hi;
+        const unsigned b = __ballot_sync(0xffffffffu, loc);
+        if (loc) {
+            const int slot = base + __popc(b & ((1u << lane) - 1u));
+            u.list[slot] = e - p.e_lo;
+            u.slot_of[e] = slot;
+        }
+        base += __popc(b);
+    }
+    const int n_local = base;
+    int nsh = 0;
+    for (int b2 = 0; b2 < p.S; ++b2) {
+        if (b2 % p.ep_size != p.ep_rank) continue;
+        const int slot = n_local + nsh;
+        if (lane == 0) u.list[slot] = (p.e_hi - p.e_lo) + nsh;
+        if (lane < kMaxT) u.rank[slot][lane] = lane < p.T ? (signed char)(p.k_top + b2) : (signed char)-1;
+        ++nsh;
+    }
+    for (int i = lane; i < n_local * kMaxT; i += 32) u.rank[i / kMaxT][i % kMaxT] = -1;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int i = lane + 32 * j;
+        const int e = ev[j];
+        if (e >= p.e_lo && e < p.e_hi) u.rank[u.slot_of[e]][i / p.k_top] = (signed char)(i % p.k_top);
+    }
+    if (lane == 0) {
+        u.count = n_local + nsh;
+        u.union_size = __popcll(m0) + __popcll(m1);
+    }
+    __syncwarp();
+}
+
+// CTA 0 of the gate/up launch publishes the union for the accept kernel,
+// telemetry and the debug taps.
+__device__ __forceinline__ void publish_union(const GemvParams& p, const UnionSmem& u) {
+    for (int i = threadIdx.x; i < u.count * kMaxT; i += blockDim.x)
+        p.route_rank[i] = u.rank[i / kMaxT][i % kMaxT];
+    for (int i = threadIdx.x; i < u.count; i += blockDim.x) p.list[i] = u.list[i];
+    if (threadIdx.x == 0) {
+        *p.count = u.count;
+        *p.union_size = u.union_size;
+    }
+}
 
 
 __device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
 
 template <int NT, int EPI>
 __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, int bl, int st, int lane,
-                                              float (&acc)[kTPW][NT][4]) {
+                                              float (&acc)[kTPW][NT][4], const signed char* rr) {
     const int g = lane >> 2, t = lane & 3;
     if constexpr (EPI == EPI_STORE || EPI == EPI_ADD) {
 #pragma unroll
@@ -111,7 +203,6 @@ __device__ __forceinline__ void gemv_epilogue(const GemvParams& p, int bl, int s
             }
         }
     } else if constexpr (EPI == EPI_DOWN) {
-        const int* rr = p.route_rank + bl * kMaxT;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
@@ -220,6 +311,9 @@ template <int NT, int EPI>
 __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams p) {
     extern __shared__ float4 red[];  // [warp][slot][kTPW*NT*32]
     __shared__ long long seg_unit[kGemvWarps][2];
+    __shared__ UnionSmem un;
+    const bool routed = p.topk_id != nullptr;
+    auto rk_row = [&](int bl) -> const signed char* { return routed ? un.rank[bl] : nullptr; };
     constexpr int kSlot = kTPW * NT * 32;
     constexpr int kUnroll = NT == 1 ? 4 : 3;
     const int lane = threadIdx.x & 31;
@@ -232,13 +326,19 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     // (attention combine / expert combine) is still finishing.
     uint4 a[kUnroll][kTPW];
     bool pre = false;
-    const bool dense = p.list == nullptr && p.count == nullptr;
+    const bool dense = !routed && p.list == nullptr && p.count == nullptr;
+    if (routed && p.early_list) {
+        // the router's top-k was written two kernels back (final): build the
+        // union now so the prologue can address the first expert weights
+        if (warp == 0) build_union(p, un);
+        __syncthreads();
+    }
     if (dense || p.early_list) {
         // weights addressable now: dense matrices always; the expert down
         // projection because its active list was written two kernels back
         // and the gate/up kernel triggers its dependents only after its own
         // griddepcontrol.wait.
-        const int U0 = dense ? p.n_blocks : __ldcg(p.count);
+        const int U0 = dense ? p.n_blocks : (routed ? un.count : __ldcg(p.count));
         const long long total0 = (long long)U0 * p.n_st * p.n_ks;
         long long ncm = total0 / ((long long)p.min_seg * kGemvWarps);
         if (ncm < 1) ncm = 1;
@@ -255,7 +355,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
             if (ks10 - ks00 >= kUnroll) {
                 const int bl0 = (int)(unit0 / p.n_st);
                 const int st0 = (int)(unit0 - (long long)bl0 * p.n_st);
-                const int blk0 = p.list ? __ldcg(p.list + bl0) : bl0;
+                const int blk0 = routed ? un.list[bl0] : (p.list ? __ldcg(p.list + bl0) : bl0);
                 const uint4* A0 = p.W + (long long)blk0 * p.w_block_stride +
                                   (long long)st0 * p.n_ks * (kTPW * 32) + lane;
 #pragma unroll
@@ -275,7 +375,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
                     if (whi0 - pos < n) n = whi0 - pos;
                     const int bl = (int)(unit / p.n_st);
                     const int st = (int)(unit - (long long)bl * p.n_st);
-                    const int blk = p.list ? __ldcg(p.list + bl) : bl;
+                    const int blk = routed ? un.list[bl] : (p.list ? __ldcg(p.list + bl) : bl);
                     const char* src = reinterpret_cast<const char*>(
                         p.W + (long long)blk * p.w_block_stride + ((long long)st * p.n_ks + ks) * (kTPW * 32));
                     const unsigned long long bytes = (unsigned long long)n * kTPW * 32 * 16;
@@ -293,7 +393,12 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     if (p.trigger) griddep_launch();
     CTA_TRACE(p.trace);
     if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
-    const int U = p.count ? *p.count : p.n_blocks;
+    if (routed && !p.early_list) {
+        if (warp == 0) build_union(p, un);
+        __syncthreads();
+    }
+    if (routed && p.publish && blockIdx.x == 0) publish_union(p, un);
+    const int U = routed ? un.count : (p.count ? *p.count : p.n_blocks);
     const long long per_block = (long long)p.n_st * p.n_ks;
     const long long total = (long long)U * per_block;
     if (total <= 0) return;
@@ -320,7 +425,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
         const int bl = (int)(unit / p.n_st);
         const int st = (int)(unit - (long long)bl * p.n_st);
-        const int blk = p.list ? p.list[bl] : bl;
+        const int blk = routed ? un.list[bl] : (p.list ? p.list[bl] : bl);
         const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
         const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
         zero_acc<NT>(acc);
@@ -361,7 +466,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         const bool first_seg = pos == wlo;
         pos += ks1 - ks0;
         if (ks0 == 0 && ks1 == p.n_ks) {
-            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
         } else {
             const int slot = first_seg ? 0 : 1;
             store_acc<NT>(red + (warp * 2 + slot) * kSlot + lane, acc, false);
@@ -386,7 +491,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         const int bl = (int)(unit / p.n_st);
         const int st = (int)(unit - (long long)bl * p.n_st);
         if (ustart >= clo && uend <= chi) {
-            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
             continue;
         }
         // crosses a CTA boundary: publish the CTA partial; last CTA reduces
@@ -404,7 +509,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         for (int j = first; j <= last; ++j)
             add_acc<NT>(acc, p.partial + ((long long)j * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
         if (lane == 0) p.counters[unit] = 0;
-        gemv_epilogue<NT, EPI>(p, bl, st, lane, acc);
+        gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
     }
 }
 

@@ -20,8 +20,6 @@
 //   (next layer's attention input, or the final norm).
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 #include "gemv_umma.cuh"
 
@@ -52,15 +50,9 @@ struct RouteParams {
     const uint16_t* router_w;    // [E + shared_gate][d] bf16
     uint16_t* xn_bfrag;          // out: MoE input, B-frag
     float* logits;               // out: [T][E+1]
-    float* logit_part;           // scratch: [T][n_slices][E+1] per-slice partial logits
-    int* ticket;                 // zero between launches
     int* topk_id;                // out: [T][k]
     float* topk_w;               // out: [T][k]
     float* gsh;                  // out: [T] shared-expert gate (1 if no gate)
-    int* list;                   // out: active local block ids [U + S_local]
-    int* count;                  // out: number of active local blocks
-    int* route_rank;             // out: [slot][16]
-    int* union_size;             // out: unique routed experts this layer (global)
     float* ycontrib;             // [T][k+S][d], zeroed for non-local entries (EP)
     uint16_t* tap_xn;            // optional [T][d]
     int T, d, E, k, S, renorm, shared_gate;
@@ -79,8 +71,26 @@ constexpr int kRowThreads = 512;            // route / combine: one CTA per toke
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
 
-// grid = T CTAs = one thread-block cluster (T <= 16, non-portable size);
-// CTA t = token t = cluster rank t.
+// Eight consecutive columns k0..k0+7 (k0 % 8 == 0) of token t, as packed
+// bf16 pairs, into a B-operand buffer with wide stores: one 16-byte store
+// in the UMMA B layout (the 8 columns are contiguous there), four 4-byte
+// stores in the mma.sync B-frag layout (pair 2q goes to lane g*4+q).
+// Narrow scattered 2-byte stores from a single CTA cost ~4 us per row.
+__device__ __forceinline__ void store_b8(uint16_t* dst, bool umma, int t, int k0, const uint32_t (&w)[4]) {
+    if (umma) {
+        *reinterpret_cast<uint4*>(dst + umma_b_index(t, k0)) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint32_t*>(dst + bfrag_index(t, k0 + 2 * q)) = w[q];
+    }
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    return (uint32_t)bf16_bits(lo) | ((uint32_t)bf16_bits(hi) << 16);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// grid = T independent CTAs, CTA t = token t:
 //  * before griddepcontrol.wait (independent of the predecessor): the
 //    router weights (when they fit, e.g. Mixtral's 72 KB) are staged in
 //    shared memory and the norm weights loaded;
@@ -88,27 +98,17 @@ constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up 
 //    for the expert GEMVs, and fp32 in smem), router logits (warp per
 //    expert row, fixed lane order), softmax and top-k (larger logit first,
 //    lower expert index on ties), gate weights (renormalised over the k for
-//    Mixtral);
-//  * cluster barrier; rank 0 gathers every token's top-k and 128-bit
-//    expert mask through distributed shared memory and builds the union:
-//    ascending unique-expert list, per-expert token ranks, shared blocks on
-//    top.  No global atomics or fences, no second kernel.
-// This is the real counterpart of the reference's stand-ins draw_expert_set
-// / sample_active_experts (expert_model.hpp:100-139): union = distinct
-// routed experts, shared blocks always active on top.
-__global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
+//    Mixtral).
+// The expert union over the T tokens is built by each CTA of the expert
+// GEMVs from topk_id (gemv.cuh build_union), so the router needs no
+// cross-CTA synchronisation: a cluster barrier costs a GPU-scope memory
+// fence (MEMBAR.ALL.GPU, ~1 us) per use.
+__global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p) {
     extern __shared__ __align__(16) unsigned char rsm[];
     float* xs = reinterpret_cast<float*>(rsm);                         // [d] MoE input (bf16 values)
     const uint16_t* wsm = reinterpret_cast<const uint16_t*>(rsm + (size_t)p.d * 4);  // staged router rows
     __shared__ float red[32];
     __shared__ float s_lg[kMaxExperts + 1];
-    __shared__ int s_mytopk[kMaxTopK];
-    __shared__ unsigned long long s_mymask[2];
-    __shared__ int s_topk[kMaxT * kMaxTopK];
-    __shared__ unsigned long long masks[kMaxT][2];
-    __shared__ int s_warp_on[kMaxExperts / 32];
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
     const int t = blockIdx.x;
     const int n_rows = p.E + (p.shared_gate ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,39 +119,61 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         uint4* dst = reinterpret_cast<uint4*>(rsm + (size_t)p.d * 4);
         for (int i = threadIdx.x; i < n_rows * p.d / 8; i += kRowThreads) dst[i] = __ldg(src + i);
     }
+    constexpr int kPreIt = 8;  // 256 columns per chunk
+    uint4 pre0[kPreIt];
+    if (!staged) {
+        // first chunk of this warp's first row: a constant, requested now
+        const uint4* w0 = reinterpret_cast<const uint4*>(p.router_w + (size_t)(warp < n_rows ? warp : 0) * p.d);
+#pragma unroll
+        for (int j = 0; j < kPreIt; ++j) {
+            const int i = lane + 32 * j;
+            pre0[j] = i < p.d / 8 ? __ldg(w0 + i) : make_uint4(0, 0, 0, 0);
+        }
+    }
+    uint4 nw[2];  // norm weights of this thread's 8-column groups
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        nw[j] = c < (p.d >> 3) ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
+    }
     griddep_wait();
     griddep_launch_early();
     CTA_TRACE(p.trace);
     if (t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
     phase_stamp(p.trace, 0);
-    // ---- norm
-    const float* x = p.x + (long long)t * p.d;
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-    constexpr int kV = 4;  // float4 per thread, d <= 8192
-    float4 xv[kV];
-#pragma unroll
-    for (int j = 0; j < kV; ++j) {
-        const int i = threadIdx.x + j * kRowThreads;
-        xv[j] = i < (p.d >> 2) ? x4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    // ---- norm: thread owns groups of 8 consecutive columns (wide loads/stores)
+    const float4* x4 = reinterpret_cast<const float4*>(p.x + (long long)t * p.d);
+    constexpr int kG = 2;  // d <= 8192
+    const int n8 = p.d >> 3;
+    float4 xv[kG][2];
     float ss = 0.f;
 #pragma unroll
-    for (int j = 0; j < kV; ++j) ss += xv[j].x * xv[j].x + xv[j].y * xv[j].y + xv[j].z * xv[j].z + xv[j].w * xv[j].w;
+    for (int j = 0; j < kG; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            xv[j][h] = c < n8 ? x4[2 * c + h] : make_float4(0.f, 0.f, 0.f, 0.f);
+            ss += xv[j][h].x * xv[j][h].x + xv[j][h].y * xv[j][h].y + xv[j][h].z * xv[j][h].z +
+                  xv[j][h].w * xv[j][h].w;
+        }
+    }
     ss = block_sum(ss, red);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
 #pragma unroll
-    for (int j = 0; j < kV; ++j) {
-        const int i = threadIdx.x + j * kRowThreads;
-        if (i >= (p.d >> 2)) continue;
-        const float vv[4] = {xv[j].x, xv[j].y, xv[j].z, xv[j].w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int c = 4 * i + q;
-            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[c]));
-            p.xn_bfrag[bfrag_index(t, c)] = b;
-            if (p.tap_xn) p.tap_xn[(long long)t * p.d + c] = b;
-            xs[c] = bits_to_f32(b);
-        }
+    for (int j = 0; j < kG; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c >= n8) continue;
+        const float4 a = xv[j][0], b = xv[j][1];
+        uint32_t w[4];
+        w[0] = pack_bf16((a.x * rinv) * bf16_lo(nw[j].x), (a.y * rinv) * bf16_hi(nw[j].x));
+        w[1] = pack_bf16((a.z * rinv) * bf16_lo(nw[j].y), (a.w * rinv) * bf16_hi(nw[j].y));
+        w[2] = pack_bf16((b.x * rinv) * bf16_lo(nw[j].z), (b.y * rinv) * bf16_hi(nw[j].z));
+        w[3] = pack_bf16((b.z * rinv) * bf16_lo(nw[j].w), (b.w * rinv) * bf16_hi(nw[j].w));
+        store_b8(p.xn_bfrag, false, t, 8 * c, w);
+        if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+        float4* xs4 = reinterpret_cast<float4*>(xs + 8 * c);
+        xs4[0] = make_float4(bf16_lo(w[0]), bf16_hi(w[0]), bf16_lo(w[1]), bf16_hi(w[1]));
+        xs4[1] = make_float4(bf16_lo(w[2]), bf16_hi(w[2]), bf16_lo(w[3]), bf16_hi(w[3]));
     }
     if (p.zero_nonlocal) {
         // EP: every (token, rank) row is written by exactly one rank's down
@@ -162,28 +184,76 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
     __syncthreads();
     phase_stamp(p.trace, 1);
     // ---- router logits: warp per expert row, lane-strided 8-element pieces
-    for (int e = warp; e < n_rows; e += kRowWarps) {
-        const uint4* w4 = staged ? reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d)
-                                 : reinterpret_cast<const uint4*>(p.router_w + (size_t)e * p.d);
-        float acc = 0.f;
-#pragma unroll 8
-        for (int i = lane; i < p.d / 8; i += 32) {
-            const uint4 w = staged ? w4[i] : __ldg(w4 + i);
-            const float4 a = reinterpret_cast<const float4*>(xs)[2 * i];
-            const float4 b = reinterpret_cast<const float4*>(xs)[2 * i + 1];
-            acc = fmaf(a.x, __uint_as_float(w.x << 16), acc);
-            acc = fmaf(a.y, __uint_as_float(w.x & 0xFFFF0000u), acc);
-            acc = fmaf(a.z, __uint_as_float(w.y << 16), acc);
-            acc = fmaf(a.w, __uint_as_float(w.y & 0xFFFF0000u), acc);
-            acc = fmaf(b.x, __uint_as_float(w.z << 16), acc);
-            acc = fmaf(b.y, __uint_as_float(w.z & 0xFFFF0000u), acc);
-            acc = fmaf(b.z, __uint_as_float(w.w << 16), acc);
-            acc = fmaf(b.w, __uint_as_float(w.w & 0xFFFF0000u), acc);
-        }
+    //      (the same per-lane order for staged and global rows)
+    auto dot8 = [&](const uint4& w, int i, float acc) {
+        const float4 a = reinterpret_cast<const float4*>(xs)[2 * i];
+        const float4 b = reinterpret_cast<const float4*>(xs)[2 * i + 1];
+        acc = fmaf(a.x, __uint_as_float(w.x << 16), acc);
+        acc = fmaf(a.y, __uint_as_float(w.x & 0xFFFF0000u), acc);
+        acc = fmaf(a.z, __uint_as_float(w.y << 16), acc);
+        acc = fmaf(a.w, __uint_as_float(w.y & 0xFFFF0000u), acc);
+        acc = fmaf(b.x, __uint_as_float(w.z << 16), acc);
+        acc = fmaf(b.y, __uint_as_float(w.z & 0xFFFF0000u), acc);
+        acc = fmaf(b.z, __uint_as_float(w.w << 16), acc);
+        acc = fmaf(b.w, __uint_as_float(w.w & 0xFFFF0000u), acc);
+        return acc;
+    };
+    auto emit = [&](int e, float acc) {
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
             s_lg[e] = acc;
             p.logits[t * (p.E + 1) + e] = acc;
+        }
+    };
+    // n8 = d / 8 column groups (declared with the norm)
+    if (staged) {
+        for (int e = warp; e < n_rows; e += kRowWarps) {
+            const uint4* w4 = reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d);
+            float acc = 0.f;
+#pragma unroll 8
+            for (int i = lane; i < n8; i += 32) acc = dot8(w4[i], i, acc);
+            emit(e, acc);
+        }
+    } else {
+        // rows from global, two per warp at a time with every load of a
+        // 256-column chunk issued before any FMA; the first chunk of the
+        // first row was requested before griddepcontrol.wait (pre0).
+        bool first = true;
+        for (int e0 = warp; e0 < n_rows; e0 += 2 * kRowWarps) {
+            const int e1 = e0 + kRowWarps;
+            const bool has1 = e1 < n_rows;
+            const uint4* w0 = reinterpret_cast<const uint4*>(p.router_w + (size_t)e0 * p.d);
+            const uint4* w1 = reinterpret_cast<const uint4*>(p.router_w + (size_t)(has1 ? e1 : e0) * p.d);
+            float a0 = 0.f, a1 = 0.f;
+            for (int c0 = 0; c0 < n8; c0 += 32 * kPreIt) {
+                uint4 r0[kPreIt], r1[kPreIt];
+                if (first) {
+#pragma unroll
+                    for (int j = 0; j < kPreIt; ++j) {
+                        const int i = c0 + lane + 32 * j;
+                        r0[j] = pre0[j];
+                        r1[j] = i < n8 ? __ldg(w1 + i) : make_uint4(0, 0, 0, 0);
+                    }
+                    first = false;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kPreIt; ++j) {
+                        const int i = c0 + lane + 32 * j;
+                        r0[j] = i < n8 ? __ldg(w0 + i) : make_uint4(0, 0, 0, 0);
+                        r1[j] = i < n8 ? __ldg(w1 + i) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kPreIt; ++j) {
+                    const int i = c0 + lane + 32 * j;
+                    if (i < n8) {
+                        a0 = dot8(r0[j], i, a0);
+                        a1 = dot8(r1[j], i, a1);
+                    }
+                }
+            }
+            emit(e0, a0);
+            if (has1) emit(e1, a1);
         }
     }
     __syncthreads();
@@ -206,7 +276,6 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
         for (int q = 0; q < kMaxExperts / 32; ++q)
             if (lane + 32 * q < p.E) z += __expf(v[q] - m);
         for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-        unsigned long long m0 = 0, m1 = 0;
         float zk = 0.f;
         float my_e = 0.f;  // lane r keeps the r-th choice
         int my_i = 0;
@@ -238,81 +307,15 @@ __global__ void __launch_bounds__(kRowThreads) moe_route_kernel(RouteParams p) {
                 my_e = ex;
                 my_i = bi;
             }
-            if (bi < 64) m0 |= 1ull << bi;
-            else m1 |= 1ull << (bi - 64);
         }
         const float den = p.renorm ? zk : z;
         if (lane < p.k) {
-            s_mytopk[lane] = my_i;
             p.topk_id[tt * p.k + lane] = my_i;
             p.topk_w[tt * p.k + lane] = my_e / den;
         }
-        if (lane == 0) {
-            p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-lg[p.E])) : 1.0f;
-            s_mymask[0] = m0;
-            s_mymask[1] = m1;
-        }
+        if (lane == 0) p.gsh[tt] = p.shared_gate ? 1.0f / (1.0f + __expf(-lg[p.E])) : 1.0f;
     }
     phase_stamp(p.trace, 3);
-    cluster.sync();  // every token's top-k and mask visible cluster-wide
-    phase_stamp(p.trace, 4);
-    if (cluster.block_rank() != 0) {
-        cluster.sync();  // keep this CTA's shared memory alive until rank 0 has read it
-        return;
-    }
-    // ---- expert union (rank 0): gather through distributed shared memory
-    for (int q = threadIdx.x; q < p.T * p.k; q += kRowThreads) {
-        const int tt = q / p.k, r = q - tt * p.k;
-        s_topk[q] = cluster.map_shared_rank(s_mytopk, tt)[r];
-    }
-    if (threadIdx.x < 2 * p.T) {
-        const int tt = threadIdx.x >> 1, h = threadIdx.x & 1;
-        masks[tt][h] = cluster.map_shared_rank(s_mymask, tt)[h];
-    }
-    __syncthreads();
-    cluster.sync();  // peers may exit now
-    phase_stamp(p.trace, 5);
-    // thread e owns expert e; ballots give ascending slots
-    unsigned long long u0 = 0, u1 = 0;
-    for (int tt = 0; tt < p.T; ++tt) {
-        u0 |= masks[tt][0];
-        u1 |= masks[tt][1];
-    }
-    const int ue = threadIdx.x;
-    const bool in_union = ue < p.E && (ue < 64 ? ((u0 >> ue) & 1ull) : ((u1 >> (ue - 64)) & 1ull));
-    const bool local_on = in_union && ue >= p.e_lo && ue < p.e_hi;
-    const unsigned ball = __ballot_sync(0xffffffffu, local_on);
-    if (lane == 0 && warp < kMaxExperts / 32) s_warp_on[warp] = __popc(ball);
-    __syncthreads();
-    int base = 0;
-    for (int w = 0; w < warp && w < kMaxExperts / 32; ++w) base += s_warp_on[w];
-    int n_local = 0;
-    for (int w = 0; w < kMaxExperts / 32; ++w) n_local += s_warp_on[w];
-    if (local_on) {
-        const int slot = base + __popc(ball & ((1u << lane) - 1u));
-        p.list[slot] = ue - p.e_lo;
-        for (int tt = 0; tt < kMaxT; ++tt) {
-            int rank = -1;
-            if (tt < p.T)
-                for (int r = 0; r < p.k; ++r)
-                    if (s_topk[tt * p.k + r] == ue) rank = r;
-            p.route_rank[slot * kMaxT + tt] = rank;
-        }
-    }
-    if (threadIdx.x == 0) {
-        *p.union_size = __popcll(u0) + __popcll(u1);
-        const int n_local_routed = p.e_hi - p.e_lo;
-        int n = n_local, lb = 0;
-        for (int b2 = 0; b2 < p.S; ++b2) {
-            if (b2 % p.ep_size != p.ep_rank) continue;
-            p.list[n] = n_local_routed + lb;
-            for (int tt = 0; tt < kMaxT; ++tt) p.route_rank[n * kMaxT + tt] = tt < p.T ? p.k + b2 : -1;
-            ++n;
-            ++lb;
-        }
-        *p.count = n;
-    }
-    phase_stamp(p.trace, 6);
 }
 
 struct CombineParams {
@@ -335,85 +338,95 @@ struct CombineParams {
     unsigned long long* trace;
 };
 
-// grid = T CTAs of 1024 threads, one token row each, a single pass with
-// every load issued up front: residual += sum_r w[t][r] * Y[t][r]
-// (+ shared-gate * sum_b Y[t][k+b]) in fixed order, then the next RMSNorm
-// (next layer's attention input, or the final norm) of the updated row.
-__global__ void __launch_bounds__(kRowThreads) moe_combine_kernel(CombineParams p) {
+// grid = T CTAs of 512 threads, one token row each; thread owns groups of
+// 8 consecutive columns (d <= 8192), every load issued up front:
+// residual += sum_r w[t][r] * Y[t][r] (+ shared-gate * sum_b Y[t][k+b]) in
+// fixed order, then the next RMSNorm (next layer's attention input, or the
+// final norm) of the updated row, stored with 16-byte stores.
+__global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombineParams p) {
     __shared__ float red[32];
     const int t = blockIdx.x;
+    constexpr int kG = 2;  // 8-column groups per thread
+    const int n8 = p.d >> 3;
+    uint4 nw[kG];          // norm weights: constants, loaded before the dependency wait
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        nw[j] = c < n8 ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
+    }
     griddep_wait();
     griddep_launch_early();
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     phase_stamp(p.trace, 0);
-    constexpr int kV = 4;  // float4 per thread, d <= 8192
-    const int n4 = p.d >> 2;
     const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
     float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
-    const float g = __ldg(p.gsh + t);
-    float4 nx[kV];
+    const int n4 = p.d >> 2;
+    const int nr = p.k + p.S;
+    const float g = p.gsh[t];
+    float4 nx[kG][2];
     float ss = 0.f;
 #pragma unroll
-    for (int j = 0; j < kV; ++j) {
-        const int i = threadIdx.x + j * kRowThreads;
-        if (i >= n4) {
-            nx[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-            continue;
-        }
-        const float4 x0 = x4[i];
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
-        const int nr = p.k + p.S;
-        for (int r0 = 0; r0 < nr; r0 += 4) {  // loads in batches of 4 rows, sums in row order
-            float4 yb[4];
+    for (int j = 0; j < kG; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c >= n8) continue;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (r0 + q < nr) yb[q] = y4[(long long)(r0 + q) * n4 + i];
+        for (int h = 0; h < 2; ++h) {
+            const int i = 2 * c + h;
+            const float4 x0 = x4[i];
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r0 = 0; r0 < nr; r0 += 4) {  // loads in batches of 4 rows, sums in row order
+                float4 yb[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int r = r0 + q;
-                if (r < p.k) {
-                    const float w = __ldg(p.topk_w + t * p.k + r);
-                    acc.x += w * yb[q].x;
-                    acc.y += w * yb[q].y;
-                    acc.z += w * yb[q].z;
-                    acc.w += w * yb[q].w;
-                } else if (r < nr) {
-                    sh.x += yb[q].x;
-                    sh.y += yb[q].y;
-                    sh.z += yb[q].z;
-                    sh.w += yb[q].w;
+                for (int q = 0; q < 4; ++q)
+                    if (r0 + q < nr) yb[q] = y4[(long long)(r0 + q) * n4 + i];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = r0 + q;
+                    if (r < p.k) {
+                        const float w = p.topk_w[t * p.k + r];
+                        acc.x += w * yb[q].x;
+                        acc.y += w * yb[q].y;
+                        acc.z += w * yb[q].z;
+                        acc.w += w * yb[q].w;
+                    } else if (r < nr) {
+                        sh.x += yb[q].x;
+                        sh.y += yb[q].y;
+                        sh.z += yb[q].z;
+                        sh.w += yb[q].w;
+                    }
                 }
             }
+            if (p.S > 0) {
+                acc.x += g * sh.x;
+                acc.y += g * sh.y;
+                acc.z += g * sh.z;
+                acc.w += g * sh.w;
+            }
+            if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
+            const float4 v = make_float4(x0.x + acc.x, x0.y + acc.y, x0.z + acc.z, x0.w + acc.w);
+            nx[j][h] = v;
+            x4[i] = v;
+            if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = v;
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
         }
-        if (p.S > 0) {
-            acc.x += g * sh.x;
-            acc.y += g * sh.y;
-            acc.z += g * sh.z;
-            acc.w += g * sh.w;
-        }
-        if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
-        nx[j] = make_float4(x0.x + acc.x, x0.y + acc.y, x0.z + acc.z, x0.w + acc.w);
-        x4[i] = nx[j];
-        if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = nx[j];
-        ss += nx[j].x * nx[j].x + nx[j].y * nx[j].y + nx[j].z * nx[j].z + nx[j].w * nx[j].w;
     }
     phase_stamp(p.trace, 1);
     ss = block_sum(ss, red);
     phase_stamp(p.trace, 2);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
 #pragma unroll
-    for (int j = 0; j < kV; ++j) {
-        const int i = threadIdx.x + j * kRowThreads;
-        if (i >= n4) continue;
-        const float vv[4] = {nx[j].x, nx[j].y, nx[j].z, nx[j].w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int col = 4 * i + q;
-            const uint16_t b = bf16_bits((vv[q] * rinv) * bits_to_f32(p.norm_w[col]));
-            p.xn_bfrag[p.umma ? umma_b_index(t, col) : bfrag_index(t, col)] = b;
-            if (p.tap_xn) p.tap_xn[(long long)t * p.d + col] = b;
-        }
+    for (int j = 0; j < kG; ++j) {
+        const int c = threadIdx.x + j * kRowThreads;
+        if (c >= n8) continue;
+        const float4 a = nx[j][0], b = nx[j][1];
+        uint32_t w[4];
+        w[0] = pack_bf16((a.x * rinv) * bf16_lo(nw[j].x), (a.y * rinv) * bf16_hi(nw[j].x));
+        w[1] = pack_bf16((a.z * rinv) * bf16_lo(nw[j].y), (a.w * rinv) * bf16_hi(nw[j].y));
+        w[2] = pack_bf16((b.x * rinv) * bf16_lo(nw[j].z), (b.y * rinv) * bf16_hi(nw[j].z));
+        w[3] = pack_bf16((b.z * rinv) * bf16_lo(nw[j].w), (b.w * rinv) * bf16_hi(nw[j].w));
+        store_b8(p.xn_bfrag, p.umma != 0, t, 8 * c, w);
+        if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     phase_stamp(p.trace, 3);
 }
