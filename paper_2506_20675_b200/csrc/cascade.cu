@@ -511,6 +511,52 @@ static cudaError_t gemv_smem_attr() {
     return e;
 }
 
+// Cluster size for the split-K dense GEMV over n_units 128-row units: the
+// largest C <= 8 with n_units * C <= SMs whose clusters can all be resident
+// at once (one wave); 0 = use the stream-K path.
+static int pick_cluster(const cascade_model* m, int n_units, int stages) {
+    for (int C = std::min(kCMaxC, m->num_sms / std::max(n_units, 1)); C >= 2; --C) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n_units * C);
+        cfg.blockDim = dim3(kUThreads);
+        cfg.dynamicSmemBytes = dense_cluster_smem_bytes(stages);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, dense_gemv_cluster_kernel<UEPI_STORE>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        if (getenv("CASCADE_DEBUG_CLUSTER")) fprintf(stderr, "cluster C=%d: %d clusters active (need %d)\n", C, n, n_units);
+        if (n >= n_units) return C;
+    }
+    return 0;
+}
+
+static cudaError_t launch_dense_cluster(int epi, const UGemvParams& p, int C, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.n_st * C);
+    cfg.blockDim = dim3(kUThreads);
+    cfg.dynamicSmemBytes = dense_cluster_smem_bytes(p.ring_stages);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = C;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (epi == UEPI_ADD) return cudaLaunchKernelEx(&cfg, dense_gemv_cluster_kernel<UEPI_ADD>, p);
+    return cudaLaunchKernelEx(&cfg, dense_gemv_cluster_kernel<UEPI_STORE>, p);
+}
+
 // ---------------------------------------------------------------- session
 struct Taps {
     uint16_t* xn_moe = nullptr;   // [L][16][d]
@@ -571,6 +617,9 @@ struct cascade_session {
     int gemv_trigger = 1;  // early launch_dependents: the down GEMV builds its union and requests its first weights while gate/up drains
     int down_early = 1;
     int umma_prologue = 1;
+    int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
+    int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
+    int o_cluster = 0;     // same for the O projection
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -690,6 +739,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
+    if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
         const int late = v[0] == '1';
         cudaMemcpyToSymbol(g_late_trigger, &late, sizeof(late));
@@ -710,6 +760,17 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
     if (e == cudaSuccess) e = gemv_smem_attr<1>();
     if (e == cudaSuccess) e = gemv_smem_attr<2>();
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
+    if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
+    if (e == cudaSuccess) e = carve(dense_gemv_cluster_kernel<UEPI_STORE>);
+    if (e == cudaSuccess) e = carve(dense_gemv_cluster_kernel<UEPI_ADD>);
+    if (e == cudaSuccess) {
+        bool on = true;
+        if (const char* v = getenv("CASCADE_DENSE_CLUSTER")) on = v[0] == '1';
+        if (on && m->umma_qkv()) s->qkv_cluster = pick_cluster(m, D.qkvd / kURows, s->cluster_stages);
+        if (on && m->umma_o()) s->o_cluster = pick_cluster(m, D.d / kURows, s->cluster_stages);
+    }
     if (e != cudaSuccess) {
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
@@ -793,6 +854,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.partial = s->upartial;
     p.counters = s->ucounters;
     p.no_prologue = !s->umma_prologue;
+    p.ring_stages = s->cluster_stages;
     return p;
 }
 
@@ -890,7 +952,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             q.ld = D.qkvd;
             q.stamp = s->stamps + 1 + 2 * l;
             q.trace = tr(1);
-            CK(launch_ugemv(UEPI_STORE, q, m->num_sms, st));
+            if (s->qkv_cluster) CK(launch_dense_cluster(UEPI_STORE, q, s->qkv_cluster, st));
+            else CK(launch_ugemv(UEPI_STORE, q, m->num_sms, st));
         } else {
             GemvParams q = gemv_base(s, T);
             q.W = w.wqkv;
@@ -957,7 +1020,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             o.out = s->x;
             o.ld = D.d;
             o.trace = tr(4);
-            CK(launch_ugemv(UEPI_ADD, o, m->num_sms, st));
+            if (s->o_cluster) CK(launch_dense_cluster(UEPI_ADD, o, s->o_cluster, st));
+            else CK(launch_ugemv(UEPI_ADD, o, m->num_sms, st));
         } else {
             GemvParams o = gemv_base(s, T);
             o.W = w.wo;

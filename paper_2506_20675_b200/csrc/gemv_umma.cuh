@@ -116,6 +116,7 @@ struct UGemvParams {
     unsigned long long* trace; // in-graph trace slot
     unsigned long long* dbg;   // optional phase stamps (scripts/umma_probe.cu)
     int no_prologue;           // A/B: issue nothing before griddepcontrol.wait
+    int ring_stages;           // dense_gemv_cluster_kernel: ring depth (<= kCMaxStages)
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -222,7 +223,9 @@ __device__ __forceinline__ void uepilogue(const UGemvParams& p, int b, int st, i
     const int lane = threadIdx.x & 31;
     const long long row = (long long)st * kURows + r;
     if constexpr (EPI == UEPI_STORE || EPI == UEPI_ADD) {
-        for (int t = 0; t < p.T; ++t) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (t >= p.T) break;
             float* o = p.out + (long long)t * p.ld + row;
             if constexpr (EPI == UEPI_ADD) *o += v[t];
             else *o = v[t];
@@ -243,7 +246,9 @@ __device__ __forceinline__ void uepilogue(const UGemvParams& p, int b, int st, i
         }
     } else if constexpr (EPI == UEPI_DOWN) {
         const int* rr = p.route_rank + b * kMaxT;
-        for (int t = 0; t < p.T; ++t) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (t >= p.T) break;
             const int rank = rr[t];
             if (rank >= 0) p.out[((long long)t * p.n_contrib + rank) * p.ld + row] = v[t];
         }
@@ -499,6 +504,202 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0 && p.dbg) atomicMax(p.dbg + 9, globaltimer_raw());
+    if (threadIdx.x == 0) {
+        unsigned long long* c = cta_trace_slot(p.trace);
+        if (c != nullptr) c[1] = globaltimer_raw();
+    }
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    }
+}
+
+
+// ---------------------------------------------------------------- cluster split-K (dense, few units)
+// Dense matrices with fewer 128-row units than SMs (QKV, O projection) are
+// split along K inside a thread-block cluster: unit u = cluster u, CTA rank
+// r of C streams k-steps [n_ks*r/C, n_ks*(r+1)/C).  The C partial
+// accumulators are reduced through distributed shared memory instead of
+// global partials + fences + atomics (the last-arriver chain of the
+// stream-K path costs ~4 global round trips at the end of every launch):
+// every CTA sends row i of its partial to the CTA that owns row i
+// (owner = i*C/128) with st.async, completing on the owner's mbarrier, and
+// the owner sums the C partials in rank order and runs the epilogue for
+// its rows.  Deterministic; the split depends only on the matrix shape.
+constexpr int kCMaxC = 8;
+constexpr int kCMaxStages = 6;
+constexpr int kCRecvFloats = (kURows + kCMaxC) * kUTok;  // sum over ranks of owned rows * 16
+
+constexpr int dense_cluster_smem_bytes(int stages) { return stages * kUStageBytes + kCRecvFloats * 4; }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// first row owned by rank j of C (rows i with i*C/128 == j)
+__device__ __forceinline__ int owner_row0(int j, int C) { return (kURows * j + C - 1) / C; }
+
+template <int EPI>
+__global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvParams p) {
+    static_assert(EPI == UEPI_STORE || EPI == UEPI_ADD, "cluster split-K: row-local epilogues only");
+    extern __shared__ __align__(1024) unsigned char ring[];
+    const int NS = p.ring_stages;
+    float* recv = reinterpret_cast<float*>(ring + (size_t)NS * kUStageBytes);  // [src][own row][16]
+    __shared__ __align__(8) uint64_t full_bar[kCMaxStages];
+    __shared__ __align__(8) uint64_t empty_bar[kCMaxStages];
+    __shared__ __align__(8) uint64_t acc_bar;
+    __shared__ __align__(8) uint64_t recv_bar;
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int C = (int)(gridDim.x / (unsigned)p.n_st);  // cluster size
+    const int rank = (int)cluster_rank();
+    const int unit = (int)cluster_id_x();
+    const int ks_lo = p.n_ks * rank / C, ks_hi = p.n_ks * (rank + 1) / C;
+    const int my_row0 = owner_row0(rank, C), my_rows = owner_row0(rank + 1, C) - my_row0;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) {
+            mb_init(&full_bar[i], 1);
+            mb_init(&empty_bar[i], 1);
+        }
+        mb_init(&acc_bar, 1);
+        mb_init(&recv_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mb_expect_tx(&recv_bar, (uint32_t)(C * my_rows * kUTok * 4));
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(&tmem_base_sh))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    // every CTA's receive barrier is initialised before anyone can send
+    cluster_sync_relaxed();
+    const uint32_t tmem = tmem_base_sh;
+
+    if (warp == 4) {
+        // ------------------------------------------------------------ TMA producer
+        uint64_t pol_a, pol_b;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
+        const uint16_t* a_base = p.W + ((long long)unit * p.n_ks) * (kUKsA / 2);
+        const int n_stages = (ks_hi - ks_lo + kUStageKs - 1) / kUStageKs;
+        auto stage_n = [&](int i) { return min(kUStageKs, ks_hi - (ks_lo + i * kUStageKs)); };
+        // PDL prologue: the weights do not depend on the predecessor
+        const int n_pre = min(NS, n_stages);
+        if (lane == 0 && !p.no_prologue) {
+            for (int i = 0; i < n_pre; ++i) {
+                const int n = stage_n(i);
+                mb_expect_tx(&full_bar[i], (uint32_t)n * (kUKsA + kUKsB));
+                bulk_g2s(ring + (size_t)i * kUStageBytes, a_base + (long long)(ks_lo + i * kUStageKs) * (kUKsA / 2),
+                         (uint32_t)n * kUKsA, &full_bar[i], pol_a);
+            }
+        }
+        griddep_wait();
+        griddep_launch();
+        if (lane == 0) {
+            for (int i = 0; i < n_stages; ++i) {
+                const int slot = i % NS;
+                const int n = stage_n(i);
+                const int ks = ks_lo + i * kUStageKs;
+                unsigned char* dst = ring + (size_t)slot * kUStageBytes;
+                if (i >= n_pre || p.no_prologue) {
+                    if (i >= NS) mb_wait(&empty_bar[slot], ((i / NS) - 1) & 1);
+                    mb_expect_tx(&full_bar[slot], (uint32_t)n * (kUKsA + kUKsB));
+                    bulk_g2s(dst, a_base + (long long)ks * (kUKsA / 2), (uint32_t)n * kUKsA, &full_bar[slot], pol_a);
+                }
+                bulk_g2s(dst + kUStageA, p.B + (long long)ks * (kUKsB / 2), (uint32_t)n * kUKsB, &full_bar[slot], pol_b);
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------------------ MMA issuer
+        griddep_wait();
+        griddep_launch();
+        if (lane == 0) {
+            const int n_stages = (ks_hi - ks_lo + kUStageKs - 1) / kUStageKs;
+            bool first = true;
+            for (int i = 0; i < n_stages; ++i) {
+                const int slot = i % NS;
+                const int n = min(kUStageKs, ks_hi - (ks_lo + i * kUStageKs));
+                mb_wait(&full_bar[slot], (i / NS) & 1);
+                tc_fence_after();
+                const unsigned char* st = ring + (size_t)slot * kUStageBytes;
+                for (int j = 0; j < n; ++j) {
+                    const uint64_t da = umma_desc(st + j * kUKsA, 2048, 128);
+                    const uint64_t db = umma_desc(st + kUStageA + j * kUKsB, 256, 128);
+                    umma_bf16(tmem, da, db, first ? 0u : 1u);
+                    first = false;
+                }
+                umma_commit(&empty_bar[slot]);
+            }
+            umma_commit(&acc_bar);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ epilogue (warps 0-3, thread = row)
+        griddep_wait();
+        griddep_launch();
+        trace_start(p.trace);
+        if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
+        const int r = warp * 32 + lane;
+        mb_wait(&acc_bar, 0);
+        tc_fence_after();
+        float val[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), val);
+        tc_fence_before();
+        // send row r's partial to its owner
+        const int own = r * C / kURows;
+        const uint32_t laddr = su32(recv + ((size_t)rank * (owner_row0(own + 1, C) - owner_row0(own, C)) +
+                                            (r - owner_row0(own, C))) * kUTok);
+        // recv layout of owner `own`: [src rank][own rows][16]
+        const uint32_t raddr = mapa_shared(laddr, (uint32_t)own);
+        const uint32_t rbar = mapa_shared(su32(&recv_bar), (uint32_t)own);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            st_async_v4(raddr + q * 16, make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]), rbar);
+        if (r >= my_row0 && r < my_row0 + my_rows) {
+            mb_wait(&recv_bar, 0);
+            float acc[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) acc[t] = 0.f;
+            for (int src = 0; src < C; ++src) {
+                const float4* f = reinterpret_cast<const float4*>(recv + ((size_t)src * my_rows + (r - my_row0)) * kUTok);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float4 x = f[q];
+                    acc[4 * q] += x.x;
+                    acc[4 * q + 1] += x.y;
+                    acc[4 * q + 2] += x.z;
+                    acc[4 * q + 3] += x.w;
+                }
+            }
+            uepilogue<EPI>(p, 0, unit, r, acc);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long* c = cta_trace_slot(p.trace);
         if (c != nullptr) c[1] = globaltimer_raw();

@@ -191,7 +191,9 @@ def test_end_to_end_greedy_decode(tiny, K):
     shape, m, om = tiny
     clean_steps = 0
     worst = 0.0
-    for trial in range(8):
+    for trial in range(32):  # prompts until enough clean lock-step verifies (near-tie flips end a prompt early)
+        if clean_steps >= 40:
+            break
         p = prompt(24, seed=100 * K + trial)
         truth = greedy_sequence(om, p, 60)
         s = cb.Session(m, max_ctx=512, k_max=8)
