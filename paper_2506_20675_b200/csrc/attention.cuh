@@ -68,8 +68,8 @@ __device__ __forceinline__ void mma_bf16_regs(float (&c)[4], uint32_t a0, uint32
 }
 
 template <int HD>
-constexpr int attn_smem_bytes() {
-    return (2 * kAttnMaxRows + 2 * kChunk) * (HD + 8) * 2;
+constexpr int attn_smem_bytes(int qrows = kAttnMaxRows) {
+    return (2 * qrows + 2 * kChunk) * (HD + 8) * 2;
 }
 
 // Two-term bf16 operands.  q and P enter the tensor cores as hi + lo bf16
@@ -96,8 +96,9 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
     constexpr int NDT = HD / 8;       // n8 dim tiles of PV
     extern __shared__ __align__(16) uint16_t sm[];
     uint16_t* qs = sm;
-    uint16_t* qsl = qs + kAttnMaxRows * LD;
-    uint16_t* ks = qsl + kAttnMaxRows * LD;
+    const int qrows = ((p.H / p.KV) * p.T + 15) / 16 * 16;  // staged query rows (smem sized per T)
+    uint16_t* qsl = qs + qrows * LD;
+    uint16_t* ks = qsl + qrows * LD;
     uint16_t* vs = ks + kChunk * LD;
 
     const int G = p.H / p.KV;
@@ -146,48 +147,93 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         const int nkeys = is_new ? p.T : min(kChunk, ctx - key0);
 
         __syncthreads();
-        // queries (rotated at their own positions, scaled, bf16)
-        for (int e = threadIdx.x; e < n_mt * 16 * HALF; e += blockDim.x) {
-            const int r = e / HALF, i = e - r * HALF;
-            float a = 0.f, b = 0.f;
-            if (r < R) {
-                const int gi = r / p.T, t = r - gi * p.T;
-                const int h = kvh * G + gi;
-                a = p.qkv[(long long)t * QD + h * HD + i];
-                b = p.qkv[(long long)t * QD + h * HD + i + HALF];
-                rope_pair(a, b, p.rope[t * HALF + i]);
-                a *= p.scale;
-                b *= p.scale;
+        // queries (rotated at their own positions, scaled, two bf16 terms):
+        // work item = (row, 4 consecutive dims i..i+3 and their rotate_half
+        // partners i+HALF..), every global load of a batch of 4 items issued
+        // before any math (this kernel is latency-bound).
+        {
+            constexpr int Q4 = HALF / 4;
+            const int n_q = n_mt * 16 * Q4;
+            for (int e0 = 0; e0 < n_q; e0 += 4 * kAttnThreads) {
+                float4 qa[4], qb[4], ca[4], cb[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kAttnThreads + threadIdx.x;
+                    const int r = e / Q4, i = (e - r * Q4) * 4;
+                    qa[u] = qb[u] = ca[u] = cb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (e < n_q && r < R) {
+                        const int gi = r / p.T, t = r - gi * p.T;
+                        const float* q = p.qkv + (long long)t * QD + (kvh * G + gi) * HD;
+                        qa[u] = *reinterpret_cast<const float4*>(q + i);
+                        qb[u] = *reinterpret_cast<const float4*>(q + i + HALF);
+                        const float4* rp = reinterpret_cast<const float4*>(p.rope + t * HALF + i);
+                        ca[u] = rp[0];  // (cos, sin) of dims i, i+1
+                        cb[u] = rp[1];  // (cos, sin) of dims i+2, i+3
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int e = e0 + u * kAttnThreads + threadIdx.x;
+                    if (e >= n_q) continue;
+                    const int r = e / Q4, i = (e - r * Q4) * 4;
+                    float a4[4] = {qa[u].x, qa[u].y, qa[u].z, qa[u].w};
+                    float b4[4] = {qb[u].x, qb[u].y, qb[u].z, qb[u].w};
+                    const float2 cs[4] = {make_float2(ca[u].x, ca[u].y), make_float2(ca[u].z, ca[u].w),
+                                          make_float2(cb[u].x, cb[u].y), make_float2(cb[u].z, cb[u].w)};
+                    uint32_t ah[2], al[2], bh[2], bl[2];
+#pragma unroll
+                    for (int k2 = 0; k2 < 4; ++k2) {
+                        rope_pair(a4[k2], b4[k2], cs[k2]);
+                        a4[k2] *= p.scale;
+                        b4[k2] *= p.scale;
+                    }
+                    split_bf16x2(a4[0], a4[1], ah[0], al[0]);
+                    split_bf16x2(a4[2], a4[3], ah[1], al[1]);
+                    split_bf16x2(b4[0], b4[1], bh[0], bl[0]);
+                    split_bf16x2(b4[2], b4[3], bh[1], bl[1]);
+                    *reinterpret_cast<uint2*>(qs + r * LD + i) = make_uint2(ah[0], ah[1]);
+                    *reinterpret_cast<uint2*>(qs + r * LD + i + HALF) = make_uint2(bh[0], bh[1]);
+                    *reinterpret_cast<uint2*>(qsl + r * LD + i) = make_uint2(al[0], al[1]);
+                    *reinterpret_cast<uint2*>(qsl + r * LD + i + HALF) = make_uint2(bl[0], bl[1]);
+                }
             }
-            const uint16_t ah = bf16_bits(a), bh = bf16_bits(b);
-            qs[r * LD + i] = ah;
-            qs[r * LD + i + HALF] = bh;
-            qsl[r * LD + i] = bf16_bits(a - bits_to_f32(ah));
-            qsl[r * LD + i + HALF] = bf16_bits(b - bits_to_f32(bh));
         }
         if (is_new) {
-            for (int e = threadIdx.x; e < kChunk * HALF; e += blockDim.x) {
-                const int j = e / HALF, i = e - j * HALF;
-                uint16_t ka = 0, kb = 0, va = 0, vb = 0;
+            // the T new keys (rotated) and values -> bf16, appended to the
+            // cache and staged; rows T..kChunk-1 are zero
+            constexpr int Q4 = HALF / 4;
+            for (int e = threadIdx.x; e < kChunk * Q4; e += kAttnThreads) {
+                const int j = e / Q4, i = (e - j * Q4) * 4;
+                uint2 ka = make_uint2(0, 0), kb = ka, va = ka, vb = ka;
                 if (j < p.T) {
                     const float* kr = p.qkv + (long long)j * QD + p.H * HD + kvh * HD;
                     const float* vr = p.qkv + (long long)j * QD + (p.H + p.KV) * HD + kvh * HD;
-                    float a = kr[i], b = kr[i + HALF];
-                    rope_pair(a, b, p.rope[j * HALF + i]);
-                    ka = bf16_bits(a);
-                    kb = bf16_bits(b);
-                    va = bf16_bits(vr[i]);
-                    vb = bf16_bits(vr[i + HALF]);
+                    const float4 k0 = *reinterpret_cast<const float4*>(kr + i);
+                    const float4 k1 = *reinterpret_cast<const float4*>(kr + i + HALF);
+                    const float4 v0 = *reinterpret_cast<const float4*>(vr + i);
+                    const float4 v1 = *reinterpret_cast<const float4*>(vr + i + HALF);
+                    const float4* rp = reinterpret_cast<const float4*>(p.rope + j * HALF + i);
+                    const float4 c0 = rp[0], c1 = rp[1];
+                    float a4[4] = {k0.x, k0.y, k0.z, k0.w};
+                    float b4[4] = {k1.x, k1.y, k1.z, k1.w};
+                    rope_pair(a4[0], b4[0], make_float2(c0.x, c0.y));
+                    rope_pair(a4[1], b4[1], make_float2(c0.z, c0.w));
+                    rope_pair(a4[2], b4[2], make_float2(c1.x, c1.y));
+                    rope_pair(a4[3], b4[3], make_float2(c1.z, c1.w));
+                    ka = make_uint2(pack_bf16x2(a4[0], a4[1]), pack_bf16x2(a4[2], a4[3]));
+                    kb = make_uint2(pack_bf16x2(b4[0], b4[1]), pack_bf16x2(b4[2], b4[3]));
+                    va = make_uint2(pack_bf16x2(v0.x, v0.y), pack_bf16x2(v0.z, v0.w));
+                    vb = make_uint2(pack_bf16x2(v1.x, v1.y), pack_bf16x2(v1.z, v1.w));
                     const long long base = ((long long)kvh * p.max_ctx + ctx + j) * HD;
-                    p.kc[base + i] = ka;
-                    p.kc[base + i + HALF] = kb;
-                    p.vc[base + i] = va;
-                    p.vc[base + i + HALF] = vb;
+                    *reinterpret_cast<uint2*>(p.kc + base + i) = ka;
+                    *reinterpret_cast<uint2*>(p.kc + base + i + HALF) = kb;
+                    *reinterpret_cast<uint2*>(p.vc + base + i) = va;
+                    *reinterpret_cast<uint2*>(p.vc + base + i + HALF) = vb;
                 }
-                ks[j * LD + i] = ka;
-                ks[j * LD + i + HALF] = kb;
-                vs[j * LD + i] = va;
-                vs[j * LD + i + HALF] = vb;
+                *reinterpret_cast<uint2*>(ks + j * LD + i) = ka;
+                *reinterpret_cast<uint2*>(ks + j * LD + i + HALF) = kb;
+                *reinterpret_cast<uint2*>(vs + j * LD + i) = va;
+                *reinterpret_cast<uint2*>(vs + j * LD + i + HALF) = vb;
             }
         } else if (!kv_pending) {
             issue_kv(item);  // later items: the copy overlaps the query staging above

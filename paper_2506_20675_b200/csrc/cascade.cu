@@ -985,11 +985,17 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ap.pf = pf ? w.wo : nullptr;
         ap.pf_bytes = pf ? D.wo_vec * 16 : 0;
         ap.trace = tr(2);
-        const int agrid = m->num_sms;
+        // smem sized for this T's query rows; as many CTAs per SM as fit the
+        // carveout (items are (chunk, kv head): 272 for OLMoE at ctx 1024)
+        const int qrows = (G * T + 15) / 16 * 16;
+        const int asm_ = D.hd == 32 ? attn_smem_bytes<32>(qrows) : D.hd == 64 ? attn_smem_bytes<64>(qrows)
+                                                                                : attn_smem_bytes<128>(qrows);
+        const int per_sm = std::max(1, std::min(4, (132 * 1024) / (asm_ + 2048)));
+        const int agrid = m->num_sms * per_sm;
         PB(2);
-        if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, attn_smem_bytes<32>(), st, true, ap));
-        else if (D.hd == 64) CK(launch_k(attn_partial_kernel<64>, agrid, kAttnThreads, attn_smem_bytes<64>(), st, true, ap));
-        else CK(launch_k(attn_partial_kernel<128>, agrid, kAttnThreads, attn_smem_bytes<128>(), st, true, ap));
+        if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, asm_, st, true, ap));
+        else if (D.hd == 64) CK(launch_k(attn_partial_kernel<64>, agrid, kAttnThreads, asm_, st, true, ap));
+        else CK(launch_k(attn_partial_kernel<128>, agrid, kAttnThreads, asm_, st, true, ap));
         PE();
         ++nk;
         AttnCombineParams cp{};
