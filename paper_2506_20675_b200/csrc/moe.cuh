@@ -489,21 +489,48 @@ __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p
         sincos((double)pos * inv, &sn, &cs);
         p.rope[t * (p.hd / 2) + i] = make_float2((float)cs, (float)sn);
     }
-    const uint16_t* e = p.embed + (long long)tok * p.d;
-    float* x = p.x + (long long)t * p.d;
+    // thread owns groups of 8 consecutive columns: 16-byte embedding loads,
+    // 32-byte residual stores, 16-byte B-layout stores (d <= 8192)
+    constexpr int kEG = 4;
+    const int n8 = p.d >> 3;
+    const uint4* e8 = reinterpret_cast<const uint4*>(p.embed + (long long)tok * p.d);
+    float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
+    uint4 ev[kEG], nw[kEG];
     float ss = 0.f;
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        const float v = bits_to_f32(e[i]);
-        x[i] = v;
-        if (p.tap_x) p.tap_x[(long long)t * p.d + i] = v;
-        ss += v * v;
+#pragma unroll
+    for (int j = 0; j < kEG; ++j) {
+        const int c = threadIdx.x + j * kRouteThreads;
+        ev[j] = c < n8 ? __ldg(e8 + c) : make_uint4(0, 0, 0, 0);
+        nw[j] = c < n8 ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kEG; ++j) {
+        const int c = threadIdx.x + j * kRouteThreads;
+        if (c >= n8) continue;
+        const float4 a = make_float4(bf16_lo(ev[j].x), bf16_hi(ev[j].x), bf16_lo(ev[j].y), bf16_hi(ev[j].y));
+        const float4 b = make_float4(bf16_lo(ev[j].z), bf16_hi(ev[j].z), bf16_lo(ev[j].w), bf16_hi(ev[j].w));
+        x4[2 * c] = a;
+        x4[2 * c + 1] = b;
+        if (p.tap_x) {
+            reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[2 * c] = a;
+            reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[2 * c + 1] = b;
+        }
+        ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w + b.x * b.x + b.y * b.y + b.z * b.z + b.w * b.w;
     }
     ss = block_sum(ss, red);
     const float rinv = 1.0f / sqrtf(ss / (float)p.d + p.eps);
-    for (int i = threadIdx.x; i < p.d; i += blockDim.x) {
-        const uint16_t b = bf16_bits((x[i] * rinv) * bits_to_f32(p.norm_w[i]));
-        p.xn_bfrag[p.umma ? umma_b_index(t, i) : bfrag_index(t, i)] = b;
-        if (p.tap_xn) p.tap_xn[(long long)t * p.d + i] = b;
+#pragma unroll
+    for (int j = 0; j < kEG; ++j) {
+        const int c = threadIdx.x + j * kRouteThreads;
+        if (c >= n8) continue;
+        uint32_t w[4];
+        const uint32_t ew[4] = {ev[j].x, ev[j].y, ev[j].z, ev[j].w};
+        const uint32_t ww[4] = {nw[j].x, nw[j].y, nw[j].z, nw[j].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            w[q] = pack_bf16((bf16_lo(ew[q]) * rinv) * bf16_lo(ww[q]), (bf16_hi(ew[q]) * rinv) * bf16_hi(ww[q]));
+        store_b8(p.xn_bfrag, p.umma != 0, t, 8 * c, w);
+        if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
