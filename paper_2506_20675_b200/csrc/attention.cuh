@@ -38,6 +38,12 @@ struct AttnParams {
     const void* pf;          // weights to prefetch into L2 (the O projection)
     unsigned long long pf_bytes;
     unsigned long long* trace;
+    // fused chunk combine: the last item of a KV head to finish merges that
+    // head's chunk partials and writes the O-projection input
+    int fused;
+    int* arrive;             // [KV] item arrivals (zero between launches)
+    uint16_t* out_bfrag;     // [T][H*hd] bf16, UMMA B layout (umma) or B-frag
+    int umma;
 };
 
 // rotate_half RoPE on the pair (i, i + hd/2)
@@ -352,6 +358,76 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                     out[0] = half ? mb : ma;
                     out[1] = half ? lb : la;
                 }
+            }
+        }
+        if (p.fused) {
+            // arrival of this item; the last of the KV head's nch+1 items
+            // merges the head's chunk partials (fixed chunk order)
+            __shared__ int s_last;
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) s_last = atomicAdd(p.arrive + kvh, 1) == nch;
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                const int nck = nch + 1;
+                float* scale = reinterpret_cast<float*>(sm);  // [R][nck] exp(m_c - M_r), then L_r at [R*nck + r]
+                float* Lr = scale + R * nck;
+                const float* base = p.part + (long long)kvh * R * p.max_chunks * (HD + 2);
+                for (int r = warp; r < R; r += kAttnThreads / 32) {
+                    const float* pr = base + (long long)r * p.max_chunks * (HD + 2);
+                    float m = -INFINITY;
+                    for (int c2 = lane; c2 < nck; c2 += 32) m = fmaxf(m, __ldcg(pr + (long long)c2 * (HD + 2)));
+                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    float l = 0.f;
+                    for (int c2 = lane; c2 < nck; c2 += 32) {
+                        const float e = __expf(__ldcg(pr + (long long)c2 * (HD + 2)) - m);
+                        scale[r * nck + c2] = e;
+                        l += __ldcg(pr + (long long)c2 * (HD + 2) + 1) * e;
+                    }
+                    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+                    if (lane == 0) Lr[r] = l;
+                }
+                __syncthreads();
+                // (row, 4 dims) per thread-item, the chunk loads of a batch of
+                // 9 chunks in flight together
+                constexpr int H4 = HD / 4;
+                for (int idx = threadIdx.x; idx < R * H4; idx += kAttnThreads) {
+                    const int r = idx / H4, i = (idx - r * H4) * 4;
+                    const float* pr = base + (long long)r * p.max_chunks * (HD + 2) + 2 + i;
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int c0 = 0; c0 < nck; c0 += 9) {
+                        float4 v9[9];
+#pragma unroll
+                        for (int u = 0; u < 9; ++u)
+                            if (c0 + u < nck) {
+                                const float* q = pr + (long long)(c0 + u) * (HD + 2);  // 8-byte aligned: two float2
+                                const float2 lo = __ldcg(reinterpret_cast<const float2*>(q));
+                                const float2 hi = __ldcg(reinterpret_cast<const float2*>(q + 2));
+                                v9[u] = make_float4(lo.x, lo.y, hi.x, hi.y);
+                            }
+#pragma unroll
+                        for (int u = 0; u < 9; ++u)
+                            if (c0 + u < nck) {
+                                const float sc = scale[r * nck + c0 + u];
+                                acc.x += v9[u].x * sc;
+                                acc.y += v9[u].y * sc;
+                                acc.z += v9[u].z * sc;
+                                acc.w += v9[u].w * sc;
+                            }
+                    }
+                    const float inv = 1.0f / Lr[r];
+                    const int gi = r / p.T, t = r - gi * p.T;
+                    const int k = (kvh * G + gi) * HD + i;
+                    const uint32_t w0 = pack_bf16x2(acc.x * inv, acc.y * inv), w1 = pack_bf16x2(acc.z * inv, acc.w * inv);
+                    if (p.umma) {
+                        *reinterpret_cast<uint2*>(p.out_bfrag + umma_b_index(t, k)) = make_uint2(w0, w1);
+                    } else {
+                        *reinterpret_cast<uint32_t*>(p.out_bfrag + bfrag_index(t, k)) = w0;
+                        *reinterpret_cast<uint32_t*>(p.out_bfrag + bfrag_index(t, k + 2)) = w1;
+                    }
+                }
+                if (threadIdx.x == 0) p.arrive[kvh] = 0;
             }
         }
     }

@@ -617,6 +617,8 @@ struct cascade_session {
     int gemv_trigger = 1;  // early launch_dependents: the down GEMV builds its union and requests its first weights while gate/up drains
     int down_early = 1;
     int umma_prologue = 1;
+    int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
+    int* attn_arrive = nullptr;
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
     int o_cluster = 0;     // same for the O projection
@@ -716,7 +718,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->hbuf, (size_t)std::max(nslots, 1) * D.f * 32)) ||
         (rc = salloc(s, &s->ycontrib, (size_t)kMaxT * (D.k + D.S) * D.d * 4)) ||
         (rc = salloc(s, &s->partial, (size_t)workers * 2 * kTPW * 2 * 32 * 16, false)) ||
-        (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
+        (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->attn_arrive, (size_t)D.KV * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
         (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
         (rc = salloc(s, &s->trace, 2048 * 8)) ||
@@ -739,6 +741,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
+    if (const char* v = getenv("CASCADE_ATTN_FUSED")) s->attn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
         const int late = v[0] == '1';
@@ -992,28 +995,39 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
                                                                                 : attn_smem_bytes<128>(qrows);
         const int per_sm = std::max(1, std::min(4, (132 * 1024) / (asm_ + 2048)));
         const int agrid = m->num_sms * per_sm;
+        // fused combine needs [R][chunks] + [R] floats of the kernel's smem
+        // and is only worth it while one CTA can keep every load in flight
+        // (<= 2 (row, 4-dim) items per thread); wider T use attn_combine
+        const bool fused = s->attn_fused && (long long)(G * T) * (s->max_chunks + 1) * 4 <= asm_ &&
+                           G * T * (D.hd / 4) <= 2 * kAttnThreads;
+        ap.fused = fused;
+        ap.arrive = s->attn_arrive;
+        ap.out_bfrag = s->attn_out;
+        ap.umma = m->umma_o();
         PB(2);
         if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, asm_, st, true, ap));
         else if (D.hd == 64) CK(launch_k(attn_partial_kernel<64>, agrid, kAttnThreads, asm_, st, true, ap));
         else CK(launch_k(attn_partial_kernel<128>, agrid, kAttnThreads, asm_, st, true, ap));
         PE();
         ++nk;
-        AttnCombineParams cp{};
-        cp.part = s->attn_part;
-        cp.ctx_ptr = &s->d_state->cache_len;
-        cp.out_bfrag = s->attn_out;
-        cp.tap = nullptr;
-        cp.T = T;
-        cp.H = D.H;
-        cp.KV = D.KV;
-        cp.hd = D.hd;
-        cp.max_chunks = s->max_chunks;
-        cp.umma = m->umma_o();
-        cp.trace = tr(3);
-        PB(3);
-        CK(launch_k(attn_combine_kernel, dim3(T, D.H), dim3(D.hd), 0, st, true, cp));
-        PE();
-        ++nk;
+        if (!fused) {
+            AttnCombineParams cp{};
+            cp.part = s->attn_part;
+            cp.ctx_ptr = &s->d_state->cache_len;
+            cp.out_bfrag = s->attn_out;
+            cp.tap = nullptr;
+            cp.T = T;
+            cp.H = D.H;
+            cp.KV = D.KV;
+            cp.hd = D.hd;
+            cp.max_chunks = s->max_chunks;
+            cp.umma = m->umma_o();
+            cp.trace = tr(3);
+            PB(3);
+            CK(launch_k(attn_combine_kernel, dim3(T, D.H), dim3(D.hd), 0, st, true, cp));
+            PE();
+            ++nk;
+        }
         (void)G;
         // O projection + residual
         PB(4);
