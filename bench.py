@@ -304,7 +304,11 @@ def run_ours(args, rank, world, local_rank):
         et = cls.get("expert_gate_up", 0.0) + cls.get("expert_down", 0.0)
         exp_bytes += eb
         exp_ns += et
+        # effective tokens/s = E[emitted] / latency under the reference's i.i.d.
+        # acceptance model (workload.hpp:80-86): E[emitted] = sum_{j=0..K} p^j
+        eff = {f"p={pa}": round(sum(pa ** j for j in range(K + 1)) / (per_k_us[K] * 1e-6), 1) for pa in (0.6, 0.8)}
         per_k[K] = {"latency_us": round(per_k_us[K], 2),
+                    "effective_tokens_per_s": eff,
                     "bytes_gb": round(b["total"] / 1e9, 3),
                     "hbm_gbs": round(b["total"] / (per_k_us[K] * 1e3), 1),
                     "roofline_frac": round(b["total"] / (per_k_us[K] * 1e3) / peak, 4),

@@ -202,6 +202,14 @@ CASCADE_API int cascade_step_trace(cascade_session* s, int K, double* ns, int32_
 CASCADE_API int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, int32_t* kind, int cap_slots,
                                        int* n_slots);
 
+/* Batch-invariant mode (default off): the expert GEMVs cut every expert
+ * block at fixed pieces instead of splitting the active range evenly
+ * (stream-K), so a token's logits are bitwise identical whatever the step
+ * width and routing of the other tokens, and greedy speculative decoding
+ * reproduces the K=0 token sequence exactly.  Costs 5-25% of expert-GEMV
+ * time.  Invalidates the captured step graphs. */
+CASCADE_API int cascade_set_batch_invariant(cascade_session* s, int on);
+
 /* Number of kernel launches one step of width K+1 performs (graph nodes
  * that are kernels). */
 CASCADE_API int cascade_step_kernel_count(cascade_session* s, int K, int* out);
@@ -249,6 +257,15 @@ typedef struct cascade_decode_cfg {
     int32_t baseline_refresh_interval, baseline_probe_len, backoff_enabled;
     int32_t injected_cost;     /* 1: replace measured time by cost_by_k[k] (K-trace parity) */
     double cost_by_k[CASCADE_MAX_TOKENS];
+    /* drafter: 0 = n-gram prompt lookup; 1 = replay of replay_tokens (the
+     * model's own greedy continuation of the prompt), each proposal kept
+     * with probability replay_p (i.i.d. acceptance as in the reference's
+     * workload model, workload.hpp:80-86) */
+    int32_t drafter;
+    int32_t n_replay;
+    const int32_t* replay_tokens;
+    double replay_p;
+    uint64_t replay_seed;
 } cascade_decode_cfg;
 
 CASCADE_API int cascade_decode(cascade_session* s, const int32_t* prompt, int n_prompt,

@@ -16,6 +16,7 @@
 #include <array>
 #include <chrono>
 #include <optional>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -108,6 +109,42 @@ private:
     int max_n_;
 };
 
+// Replay drafter: proposes the target model's own greedy continuation
+// (recorded by a K=0 run), each proposal independently corrupted with
+// probability 1 - p.  The accepted prefix then follows the reference's
+// acceptance model exactly (i.i.d. Bernoulli(p) until the first rejection,
+// workload.hpp:80-86), but measured through the real verifier, so the
+// utility controller sees real device costs at a controlled acceptance rate.
+class ReplayDrafter {
+public:
+    ReplayDrafter(std::vector<int32_t> truth, int n_prompt, double p, int vocab, uint64_t seed)
+        : truth_(std::move(truth)), n_prompt_(n_prompt), p_(p), vocab_(vocab), rng_(seed) {
+        if (p < 0.0 || p > 1.0) throw std::invalid_argument("ReplayDrafter: p must be in [0,1]");
+        if (vocab < 2) throw std::invalid_argument("ReplayDrafter: vocab must be >= 2");
+    }
+
+    std::vector<int32_t> propose(const std::vector<int32_t>& ctx, int k) {
+        std::vector<int32_t> out;
+        const long pos = static_cast<long>(ctx.size()) - n_prompt_;
+        std::uniform_real_distribution<double> u(0.0, 1.0);
+        for (int i = 0; i < k; ++i) {
+            const long j = pos + i;
+            if (j < 0 || j >= static_cast<long>(truth_.size())) break;
+            int32_t t = truth_[j];
+            if (u(rng_) >= p_) t = static_cast<int32_t>((t + 1) % vocab_);
+            out.push_back(t);
+        }
+        return out;
+    }
+
+private:
+    std::vector<int32_t> truth_;
+    int n_prompt_;
+    double p_;
+    int vocab_;
+    Rng rng_;
+};
+
 struct GpuRunOptions {
     EngineOptions engine;
     int k_limit = 8;                       // verifier K cap (session k_max)
@@ -118,7 +155,8 @@ struct GpuRunOptions {
 
 // The reference request loop (engine.hpp:115-182) over the real verifier.
 // `tokens` holds the prompt and receives the generated tokens.
-inline RequestMetrics run_request(Verifier& verifier, const NgramDrafter& drafter, const Policy& policy,
+template <typename Drafter>
+inline RequestMetrics run_request(Verifier& verifier, Drafter& drafter, const Policy& policy,
                                   std::vector<int32_t>& tokens, int output_len, const GpuRunOptions& opt = {}) {
     if (tokens.empty()) throw std::invalid_argument("run_request: empty prompt");
     if (output_len < 1) throw std::invalid_argument("run_request: output_len must be >= 1");

@@ -108,6 +108,11 @@ class DecodeCfg(ctypes.Structure):
         ("backoff_enabled", ctypes.c_int32),
         ("injected_cost", ctypes.c_int32),
         ("cost_by_k", ctypes.c_double * MAX_TOKENS),
+        ("drafter", ctypes.c_int32),
+        ("n_replay", ctypes.c_int32),
+        ("replay_tokens", ctypes.POINTER(ctypes.c_int32)),
+        ("replay_p", ctypes.c_double),
+        ("replay_seed", ctypes.c_uint64),
     ]
 
 
@@ -239,6 +244,7 @@ def lib() -> ctypes.CDLL:
             [P, ctypes.c_int, ctypes.POINTER(dbl), ctypes.POINTER(i32), ctypes.c_int, ctypes.POINTER(ctypes.c_int)],
         ),
         "cascade_enable_taps": (ctypes.c_int, [P, ctypes.c_int]),
+        "cascade_set_batch_invariant": (ctypes.c_int, [P, ctypes.c_int]),
         "cascade_read_tap": (ctypes.c_int, [P, ctypes.c_int, P, szt]),
         "cascade_read_weight": (
             ctypes.c_int,
@@ -442,6 +448,10 @@ class Session:
                                             _i32p(kind), cap, ctypes.byref(n)))
         return out[: n.value], kind[: n.value]
 
+    def set_batch_invariant(self, on: bool = True):
+        """Fixed expert-GEMV pieces: bitwise batch-invariant logits (lossless speculation)."""
+        _check(lib().cascade_set_batch_invariant(self.h, 1 if on else 0))
+
     def enable_taps(self, on: bool = True):
         _check(lib().cascade_enable_taps(self.h, 1 if on else 0))
 
@@ -494,4 +504,14 @@ def decode_cfg(policy: int = -1, max_new: int = 128, ngram_n: int = 3, **control
     if costs is not None:
         for i, v in enumerate(costs[:MAX_TOKENS]):
             c.cost_by_k[i] = float(v)
+    replay = controller.get("replay")  # (greedy continuation tokens, keep probability p, seed)
+    if replay is not None:
+        toks, p, seed = replay
+        arr = np.ascontiguousarray(toks, np.int32)
+        c._replay_keepalive = arr
+        c.drafter = 1
+        c.n_replay = len(arr)
+        c.replay_tokens = _i32p(arr)
+        c.replay_p = float(p)
+        c.replay_seed = int(seed)
     return c

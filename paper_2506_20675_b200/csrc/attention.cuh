@@ -117,20 +117,23 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         const int c = item / p.KV;
         const int kvh = item - c * p.KV;
         const int key0 = c * kChunk;
-        const int nkeys = min(kChunk, ctx - key0);
+        const int nkeys = max(0, min(kChunk, ctx - key0));  // cached keys of the chunk (the rest are new)
         constexpr int V8 = HD / 8;  // 16-byte pieces per row
         const long long base = ((long long)kvh * p.max_ctx + key0) * HD;
-        for (int e = threadIdx.x; e < kChunk * V8; e += blockDim.x) {
+        // slots >= nkeys belong to new keys (written by the item itself)
+        for (int e = threadIdx.x; e < nkeys * V8; e += blockDim.x) {
             const int j = e / V8, q = e - j * V8;
-            const bool ok = j < nkeys;
-            cp_async16(ks + j * LD + q * 8, p.kc + (ok ? base + (long long)e * 8 : 0), ok ? 16 : 0);
-            cp_async16(vs + j * LD + q * 8, p.vc + (ok ? base + (long long)e * 8 : 0), ok ? 16 : 0);
+            cp_async16(ks + j * LD + q * 8, p.kc + base + (long long)e * 8, 16);
+            cp_async16(vs + j * LD + q * 8, p.vc + base + (long long)e * 8, 16);
         }
         cp_async_commit();
     };
-    const int nch0 = (ctx + kChunk - 1) / kChunk;
+    // Chunks are 64 absolute key positions: chunk c covers [64c, 64c+64) of
+    // the cache + the T new keys, so a token's keys are grouped (and its
+    // softmax summed) identically whatever the step width (batch-invariant).
+    const int nch = (ctx + p.T + kChunk - 1) / kChunk;
     bool kv_pending = false;
-    if ((int)blockIdx.x < nch0 * p.KV) {
+    if ((int)blockIdx.x < nch * p.KV) {
         issue_kv(blockIdx.x);
         kv_pending = true;
     }
@@ -138,8 +141,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
     griddep_launch_early();
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
-    const int nch = (ctx + kChunk - 1) / kChunk;
-    const int n_items = (nch + 1) * p.KV;
+    const int n_items = nch * p.KV;
     const int QD = (p.H + 2 * p.KV) * HD;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
@@ -148,9 +150,10 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
         const int c = item / p.KV;
         const int kvh = item - c * p.KV;
-        const bool is_new = (c == nch);
-        const int key0 = is_new ? ctx : c * kChunk;
-        const int nkeys = is_new ? p.T : min(kChunk, ctx - key0);
+        const int key0 = c * kChunk;
+        const int nkeys = min(kChunk, ctx + p.T - key0);      // keys of this chunk
+        const int n_cached = max(0, min(kChunk, ctx - key0));  // the first n_cached come from the cache
+        const bool has_new = n_cached < nkeys;
 
         __syncthreads();
         // queries (rotated at their own positions, scaled, two bf16 terms):
@@ -204,14 +207,16 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 }
             }
         }
-        if (is_new) {
-            // the T new keys (rotated) and values -> bf16, appended to the
-            // cache and staged; rows T..kChunk-1 are zero
+        if (has_new) {
+            // the new keys of this chunk (positions ctx .. ctx+T-1, rotated)
+            // and their values -> bf16, appended to the cache and staged at
+            // their chunk slots; slots past the chunk's keys are zero
             constexpr int Q4 = HALF / 4;
-            for (int e = threadIdx.x; e < kChunk * Q4; e += kAttnThreads) {
-                const int j = e / Q4, i = (e - j * Q4) * 4;
+            for (int e = threadIdx.x; e < (kChunk - n_cached) * Q4; e += kAttnThreads) {
+                const int jl = n_cached + e / Q4, i = (e - (e / Q4) * Q4) * 4;  // chunk slot
+                const int j = key0 + jl - ctx;                                  // new-token index
                 uint2 ka = make_uint2(0, 0), kb = ka, va = ka, vb = ka;
-                if (j < p.T) {
+                if (jl < nkeys) {
                     const float* kr = p.qkv + (long long)j * QD + p.H * HD + kvh * HD;
                     const float* vr = p.qkv + (long long)j * QD + (p.H + p.KV) * HD + kvh * HD;
                     const float4 k0 = *reinterpret_cast<const float4*>(kr + i);
@@ -236,12 +241,13 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                     *reinterpret_cast<uint2*>(p.vc + base + i) = va;
                     *reinterpret_cast<uint2*>(p.vc + base + i + HALF) = vb;
                 }
-                *reinterpret_cast<uint2*>(ks + j * LD + i) = ka;
-                *reinterpret_cast<uint2*>(ks + j * LD + i + HALF) = kb;
-                *reinterpret_cast<uint2*>(vs + j * LD + i) = va;
-                *reinterpret_cast<uint2*>(vs + j * LD + i + HALF) = vb;
+                *reinterpret_cast<uint2*>(ks + jl * LD + i) = ka;
+                *reinterpret_cast<uint2*>(ks + jl * LD + i + HALF) = kb;
+                *reinterpret_cast<uint2*>(vs + jl * LD + i) = va;
+                *reinterpret_cast<uint2*>(vs + jl * LD + i + HALF) = vb;
             }
-        } else if (!kv_pending) {
+        }
+        if (n_cached > 0 && !kv_pending) {
             issue_kv(item);  // later items: the copy overlaps the query staging above
         }
         kv_pending = false;
@@ -285,7 +291,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 for (int q = 0; q < 4; ++q) {
                     const int j = n * 8 + 2 * t4 + (q & 1);
                     const int tt = (q < 2) ? ta : tb;
-                    const bool ok = j < nkeys && (!is_new || j <= tt);
+                    const bool ok = j < nkeys && key0 + j <= ctx + tt;  // causal on absolute positions
                     if (!ok) s[n][q] = -INFINITY;
                     if (q < 2) ma = fmaxf(ma, s[n][q]);
                     else mb = fmaxf(mb, s[n][q]);
@@ -361,32 +367,35 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
             }
         }
         if (p.fused) {
-            // arrival of this item; the last of the KV head's nch+1 items
+            // arrival of this item; the last of the KV head's nch items
             // merges the head's chunk partials (fixed chunk order)
             __shared__ int s_last;
             __threadfence();
             __syncthreads();
-            if (threadIdx.x == 0) s_last = atomicAdd(p.arrive + kvh, 1) == nch;
+            if (threadIdx.x == 0) s_last = atomicAdd(p.arrive + kvh, 1) == nch - 1;
             __syncthreads();
             if (s_last) {
                 __threadfence();
-                const int nck = nch + 1;
+                const int nck = nch;
                 float* scale = reinterpret_cast<float*>(sm);  // [R][nck] exp(m_c - M_r), then L_r at [R*nck + r]
-                float* Lr = scale + R * nck;
+                float* Lr = scale + R * nck;  // [R]
+                float* lv = Lr + R;           // [R][nck] chunk sums l_c
                 const float* base = p.part + (long long)kvh * R * p.max_chunks * (HD + 2);
                 for (int r = warp; r < R; r += kAttnThreads / 32) {
                     const float* pr = base + (long long)r * p.max_chunks * (HD + 2);
                     float m = -INFINITY;
                     for (int c2 = lane; c2 < nck; c2 += 32) m = fmaxf(m, __ldcg(pr + (long long)c2 * (HD + 2)));
                     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    float l = 0.f;
                     for (int c2 = lane; c2 < nck; c2 += 32) {
-                        const float e = __expf(__ldcg(pr + (long long)c2 * (HD + 2)) - m);
-                        scale[r * nck + c2] = e;
-                        l += __ldcg(pr + (long long)c2 * (HD + 2) + 1) * e;
+                        scale[r * nck + c2] = __expf(__ldcg(pr + (long long)c2 * (HD + 2)) - m);
+                        lv[r * nck + c2] = __ldcg(pr + (long long)c2 * (HD + 2) + 1);
                     }
-                    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-                    if (lane == 0) Lr[r] = l;
+                    __syncwarp();
+                    if (lane == 0) {  // sequential in chunk order (same expression as attn_combine_kernel)
+                        float l = 0.f;
+                        for (int c2 = 0; c2 < nck; ++c2) l = fmaf(lv[r * nck + c2], scale[r * nck + c2], l);
+                        Lr[r] = l;
+                    }
                 }
                 __syncthreads();
                 // (row, 4 dims) per thread-item, the chunk loads of a batch of
@@ -410,16 +419,16 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                         for (int u = 0; u < 9; ++u)
                             if (c0 + u < nck) {
                                 const float sc = scale[r * nck + c0 + u];
-                                acc.x += v9[u].x * sc;
-                                acc.y += v9[u].y * sc;
-                                acc.z += v9[u].z * sc;
-                                acc.w += v9[u].w * sc;
+                                acc.x = fmaf(v9[u].x, sc, acc.x);
+                                acc.y = fmaf(v9[u].y, sc, acc.y);
+                                acc.z = fmaf(v9[u].z, sc, acc.z);
+                                acc.w = fmaf(v9[u].w, sc, acc.w);
                             }
                     }
-                    const float inv = 1.0f / Lr[r];
+                    const float L = Lr[r];
                     const int gi = r / p.T, t = r - gi * p.T;
                     const int k = (kvh * G + gi) * HD + i;
-                    const uint32_t w0 = pack_bf16x2(acc.x * inv, acc.y * inv), w1 = pack_bf16x2(acc.z * inv, acc.w * inv);
+                    const uint32_t w0 = pack_bf16x2(acc.x / L, acc.y / L), w1 = pack_bf16x2(acc.z / L, acc.w / L);
                     if (p.umma) {
                         *reinterpret_cast<uint2*>(p.out_bfrag + umma_b_index(t, k)) = make_uint2(w0, w1);
                     } else {
@@ -460,7 +469,7 @@ __global__ void attn_combine_kernel(AttnCombineParams p) {
     const int R = G * p.T;
     const int r = gi * p.T + t;
     const int ctx = *p.ctx_ptr;
-    const int nch = (ctx + kChunk - 1) / kChunk + 1;
+    const int nch = (ctx + p.T + kChunk - 1) / kChunk;  // 64-key chunks of absolute positions (attn_partial_kernel)
     const int stride = p.hd + 2;
     const float* base = p.part + ((long long)kvh * R + r) * p.max_chunks * stride;
     // every load of the first kCB chunks is issued up front: (max, sum) of
@@ -483,28 +492,35 @@ __global__ void attn_combine_kernel(AttnCombineParams p) {
     float M = -INFINITY;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) M = fmaxf(M, red[w]);
     __syncthreads();
-    float l = 0.f;
-    if ((int)threadIdx.x < nch) {
-        const float sc = __expf(mc - M);
-        scale_c[threadIdx.x] = sc;
-        l = lc * sc;
+    // scale_c = exp(m_c - M); L = sum_c l_c * scale_c summed sequentially in
+    // chunk order (the fused combine in attn_partial_kernel computes the
+    // identical expression, so the result does not depend on the path)
+    __shared__ float s_L;
+    __shared__ float l_c[kMaxChunksSmem];
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+        scale_c[c] = __expf(base[(long long)c * stride] - M);
+        l_c[c] = base[(long long)c * stride + 1];
     }
-    for (int c = threadIdx.x + blockDim.x; c < nch; c += blockDim.x) {
-        const float sc = __expf(base[(long long)c * stride] - M);
-        scale_c[c] = sc;
-        l += base[(long long)c * stride + 1] * sc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float L0 = 0.f;
+        for (int c = 0; c < nch; ++c) L0 = fmaf(l_c[c], scale_c[c], L0);
+        s_L = L0;
     }
-    const float L = block_sum(l, red);  // syncs: scale_c visible
+    (void)mc;
+    (void)lc;
+    __syncthreads();
+    const float L = s_L;
     float o = 0.f;
 #pragma unroll
     for (int c = 0; c < kCB; ++c)
-        if (c < nch) o += ov[c] * scale_c[c];
+        if (c < nch) o = fmaf(ov[c], scale_c[c], o);
     for (int c0 = kCB; c0 < nch; c0 += kCB) {
 #pragma unroll
         for (int c = 0; c < kCB; ++c) ov[c] = c0 + c < nch ? base[(long long)(c0 + c) * stride + 2 + i] : 0.f;
 #pragma unroll
         for (int c = 0; c < kCB; ++c)
-            if (c0 + c < nch) o += ov[c] * scale_c[c0 + c];
+            if (c0 + c < nch) o = fmaf(ov[c], scale_c[c0 + c], o);
     }
     const float v = o / L;
     const int k = h * p.hd + i;

@@ -618,6 +618,7 @@ struct cascade_session {
     int down_early = 1;
     int umma_prologue = 1;
     int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
+    int invariant = 0;     // batch-invariant expert GEMV split (bitwise-lossless speculation)
     int* attn_arrive = nullptr;
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
@@ -717,7 +718,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->union_size, (size_t)D.L * 4)) ||
         (rc = salloc(s, &s->hbuf, (size_t)std::max(nslots, 1) * D.f * 32)) ||
         (rc = salloc(s, &s->ycontrib, (size_t)kMaxT * (D.k + D.S) * D.d * 4)) ||
-        (rc = salloc(s, &s->partial, (size_t)workers * 2 * kTPW * 2 * 32 * 16, false)) ||
+        (rc = salloc(s, &s->partial, (size_t)std::max<long long>(workers, (long long)nslots * s->gemv_grid) * 2 * kTPW * 2 * 32 * 16, false)) ||
         (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->attn_arrive, (size_t)D.KV * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
         (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
@@ -742,6 +743,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
     if (const char* v = getenv("CASCADE_ATTN_FUSED")) s->attn_fused = v[0] == '1';
+    if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
         const int late = v[0] == '1';
@@ -788,6 +790,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
 }
 
 extern "C" void* cascade_session_stream(cascade_session* s) { return s ? (void*)s->stream : nullptr; }
+extern "C" int cascade_internal_vocab(const cascade_session* s) { return s ? s->m->g.vocab : 0; }
 
 // ------------------------------------------------------------ step enqueue
 // Every kernel of the step is launched with programmatic stream
@@ -867,6 +870,7 @@ static GemvParams gemv_base(cascade_session* s, int T) {
     p.min_seg = 8;
     p.partial = s->partial;
     p.counters = s->counters;
+    p.invariant = s->invariant;
     p.n_blocks = 1;
     p.l2_prologue = s->l2_prologue;
     p.trigger = s->gemv_trigger;
@@ -998,7 +1002,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         // fused combine needs [R][chunks] + [R] floats of the kernel's smem
         // and is only worth it while one CTA can keep every load in flight
         // (<= 2 (row, 4-dim) items per thread); wider T use attn_combine
-        const bool fused = s->attn_fused && (long long)(G * T) * (s->max_chunks + 1) * 4 <= asm_ &&
+        const bool fused = s->attn_fused && ((long long)(G * T) * (2 * s->max_chunks + 1)) * 4 <= asm_ &&
                            G * T * (D.hd / 4) <= 2 * kAttnThreads;
         ap.fused = fused;
         ap.arrive = s->attn_arrive;
@@ -1364,6 +1368,21 @@ extern "C" int cascade_session_reset(cascade_session* s) {
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaMemset(s->d_state, 0, sizeof(DevState)));
     CK(cudaDeviceSynchronize());
+    return CASCADE_OK;
+}
+
+extern "C" int cascade_set_batch_invariant(cascade_session* s, int on) {
+    if (!s) return set_err(CASCADE_EINVAL, "bad arguments");
+    CK(cudaSetDevice(s->m->device));
+    CK(cudaStreamSynchronize(s->stream));
+    const int v = on ? 1 : 0;
+    if (v == s->invariant) return CASCADE_OK;
+    s->invariant = v;
+    for (int T = 0; T <= kMaxT; ++T)  // graphs bake the GEMV parameters: recapture lazily
+        if (s->graph[T]) {
+            cudaGraphExecDestroy(s->graph[T]);
+            s->graph[T] = nullptr;
+        }
     return CASCADE_OK;
 }
 

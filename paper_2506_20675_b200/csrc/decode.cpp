@@ -16,6 +16,7 @@
 // cascade.cu owns the thread's error slot; route messages through a tiny
 // setter it exports internally.
 extern "C" int cascade_internal_set_error(int code, const char* msg);
+extern "C" int cascade_internal_vocab(const cascade_session* s);
 
 extern "C" int cascade_decode(cascade_session* s, const int32_t* prompt, int n_prompt, const cascade_decode_cfg* cfg,
                               int32_t* out_tokens, int32_t* n_out, double* telemetry, int32_t telemetry_cap,
@@ -61,8 +62,20 @@ extern "C" int cascade_decode(cascade_session* s, const int32_t* prompt, int n_p
         opt.trace = &trace;
         std::vector<int32_t> toks(prompt, prompt + n_prompt);
         Verifier v(s);
-        NgramDrafter drafter(cfg->ngram_n);
-        const RequestMetrics m = run_request(v, drafter, policy, toks, cfg->max_new, opt);
+        RequestMetrics m;
+        if (cfg->drafter == 1) {
+            if (!cfg->replay_tokens || cfg->n_replay < 1)
+                throw std::invalid_argument("cascade_decode: replay drafter needs replay_tokens");
+            const int vocab = cascade_internal_vocab(s);
+            ReplayDrafter drafter(std::vector<int32_t>(cfg->replay_tokens, cfg->replay_tokens + cfg->n_replay), n_prompt,
+                                  cfg->replay_p, vocab, cfg->replay_seed);
+            m = run_request(v, drafter, policy, toks, cfg->max_new, opt);
+        } else if (cfg->drafter == 0) {
+            NgramDrafter drafter(cfg->ngram_n);
+            m = run_request(v, drafter, policy, toks, cfg->max_new, opt);
+        } else {
+            throw std::invalid_argument("cascade_decode: drafter must be 0 (n-gram) or 1 (replay)");
+        }
         const int gen = static_cast<int>(toks.size()) - n_prompt;
         const int cap = cfg->max_new + CASCADE_MAX_TOKENS;
         const int n = gen < cap ? gen : cap;

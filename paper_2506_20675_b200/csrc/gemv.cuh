@@ -70,6 +70,7 @@ struct GemvParams {
     int S, ep_rank, ep_size;   // shared blocks; shared block b lives on rank b % ep_size
     int publish;
     int* union_size;           // out (publish): distinct routed experts of the step
+    int invariant;             // 1: fixed pieces per block (batch-invariant sums); 0: stream-K over all blocks
 };
 
 constexpr int kGemvThreads = 256;
@@ -293,6 +294,20 @@ __device__ __forceinline__ void store_acc(float4* dst, const float (&acc)[kTPW][
         }
 }
 
+// Pieces per block: a fixed function of the block shape and the grid, so
+// every super-tile is cut at the same k-steps whatever the router chose
+// (U) and however many tokens ride along.  Sums are therefore identical
+// for a token in any verify step (batch-invariant), which makes greedy
+// speculative decoding bitwise lossless.  CTA c streams piece c of every
+// active block when P == grid (equal bytes per CTA for any U).
+__device__ __forceinline__ int block_pieces(const GemvParams& p, long long per_block) {
+    long long pm = per_block / ((long long)p.min_seg * kGemvWarps);
+    if (pm < 1) pm = 1;
+    return pm < (long long)gridDim.x ? (int)pm : (int)gridDim.x;
+}
+// Mode 0 (stream-K) treats the whole active range as one block: P = grid
+// equal contiguous pieces, one per CTA, each split among the 8 warps.
+
 template <int NT>
 constexpr int gemv_smem_bytes() {
     return kGemvWarps * 2 * kTPW * NT * 32 * 16;
@@ -339,14 +354,19 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         // and the gate/up kernel triggers its dependents only after its own
         // griddepcontrol.wait.
         const int U0 = dense ? p.n_blocks : (routed ? un.count : __ldcg(p.count));
-        const long long total0 = (long long)U0 * p.n_st * p.n_ks;
-        long long ncm = total0 / ((long long)p.min_seg * kGemvWarps);
-        if (ncm < 1) ncm = 1;
-        const int NC0 = (long long)gridDim.x < ncm ? (int)gridDim.x : (int)ncm;
-        if ((int)blockIdx.x < NC0 && total0 > 0) {
-            const long long clo0 = total0 * blockIdx.x / NC0, chi0 = total0 * (blockIdx.x + 1) / NC0;
-            const long long wlo0 = clo0 + (chi0 - clo0) * warp / kGemvWarps;
-            const long long whi0 = clo0 + (chi0 - clo0) * (warp + 1) / kGemvWarps;
+        // work blocks: each expert block (batch-invariant mode), or the whole
+        // active range as one block (stream-K: equal bytes per CTA, splits depend on U)
+        const long long pb0 = (long long)p.n_st * p.n_ks * (p.invariant ? 1 : U0);
+        const int nb0 = p.invariant ? U0 : (U0 > 0 ? 1 : 0);
+        const int P0 = block_pieces(p, pb0);
+        long long wlo0 = 0, whi0 = 0;
+        if ((int)blockIdx.x < nb0 * P0) {
+            const int b0 = (int)blockIdx.x / P0, q0 = (int)blockIdx.x - b0 * P0;
+            const long long clo0 = (long long)b0 * pb0 + pb0 * q0 / P0, chi0 = (long long)b0 * pb0 + pb0 * (q0 + 1) / P0;
+            wlo0 = clo0 + (chi0 - clo0) * warp / kGemvWarps;
+            whi0 = clo0 + (chi0 - clo0) * (warp + 1) / kGemvWarps;
+        }
+        if (whi0 > wlo0) {
             const long long unit0 = wlo0 / p.n_ks;
             const int ks00 = (int)(wlo0 - unit0 * p.n_ks);
             const long long rem0 = whi0 - wlo0;
@@ -399,107 +419,129 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     }
     if (routed && p.publish && blockIdx.x == 0) publish_union(p, un);
     const int U = routed ? un.count : (p.count ? *p.count : p.n_blocks);
-    const long long per_block = (long long)p.n_st * p.n_ks;
-    const long long total = (long long)U * per_block;
-    if (total <= 0) return;
-    long long nc_max = total / ((long long)p.min_seg * kGemvWarps);
-    if (nc_max < 1) nc_max = 1;
-    const int NC = (long long)gridDim.x < nc_max ? (int)gridDim.x : (int)nc_max;
-    const int c = blockIdx.x;
-    if (c >= NC) return;
-    const long long clo = total * c / NC, chi = total * (c + 1) / NC;
-    const long long wlo = clo + (chi - clo) * warp / kGemvWarps;
-    const long long whi = clo + (chi - clo) * (warp + 1) / kGemvWarps;
-    if (lane == 0) {
-        seg_unit[warp][0] = -1;
-        seg_unit[warp][1] = -1;
-    }
-    __syncwarp();
-
+    const long long per_block = (long long)p.n_st * p.n_ks * (p.invariant ? 1 : U);
+    const int n_blocks_w = p.invariant ? U : (U > 0 ? 1 : 0);
+    const int P = block_pieces(p, per_block);
+    const int n_items = n_blocks_w * P;
     float acc[kTPW][NT][4];
-    long long pos = wlo;
-    while (pos < whi) {
-        const long long unit = pos / p.n_ks;
-        const int ks0 = (int)(pos - unit * p.n_ks);
-        const long long rem = whi - pos;
-        const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
-        const int bl = (int)(unit / p.n_st);
-        const int st = (int)(unit - (long long)bl * p.n_st);
-        const int blk = routed ? un.list[bl] : (p.list ? p.list[bl] : bl);
-        const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
-        const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
-        zero_acc<NT>(acc);
-        int s = ks0;
-        for (; s + kUnroll <= ks1; s += kUnroll) {
-            uint2 b[kUnroll][NT];
-            if (!pre) {
+    constexpr int kMaxPend = 2 * kMaxSlots;  // <= 2 boundary super-tiles per item
+    __shared__ int4 pend[kMaxPend];
+    __shared__ int n_pend;
+    if (threadIdx.x == 0) n_pend = 0;
+    __syncthreads();
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int b = item / P, q = item - b * P;
+        // this piece of block b, in flat (unit, k-step) positions
+        const long long base = (long long)b * per_block;
+        const long long clo = base + per_block * q / P, chi = base + per_block * (q + 1) / P;
+        const long long wlo = clo + (chi - clo) * warp / kGemvWarps;
+        const long long whi = clo + (chi - clo) * (warp + 1) / kGemvWarps;
+        if (lane == 0) {
+            seg_unit[warp][0] = -1;
+            seg_unit[warp][1] = -1;
+        }
+        __syncwarp();
+
+        long long pos = wlo;
+        while (pos < whi) {
+            const long long unit = pos / p.n_ks;
+            const int ks0 = (int)(pos - unit * p.n_ks);
+            const long long rem = whi - pos;
+            const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
+            const int bl = (int)(unit / p.n_st);
+            const int st = (int)(unit - (long long)bl * p.n_st);
+            const int blk = routed ? un.list[bl] : (p.list ? p.list[bl] : bl);
+            const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
+            const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
+            zero_acc<NT>(acc);
+            int s = ks0;
+            for (; s + kUnroll <= ks1; s += kUnroll) {
+                uint2 bb[kUnroll][NT];
+                if (!pre) {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                        for (int it = 0; it < kTPW; ++it)
+                            a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+                }
+                pre = false;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) bb[u][nt] = ldg_act(Bp + ((s + u) * 2 + nt) * 32);
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
                     for (int it = 0; it < kTPW; ++it)
-                        a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], bb[u][nt]);
             }
-            pre = false;
+            for (; s < ks1; ++s) {
+                uint4 a1[kTPW];
+                uint2 bb[NT];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+                for (int it = 0; it < kTPW; ++it) a1[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) b[u][nt] = ldg_act(Bp + ((s + u) * 2 + nt) * 32);
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
+                for (int nt = 0; nt < NT; ++nt) bb[nt] = ldg_act(Bp + (s * 2 + nt) * 32);
 #pragma unroll
                 for (int it = 0; it < kTPW; ++it)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], b[u][nt]);
+                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], bb[nt]);
+            }
+            const bool first_seg = pos == wlo;
+            pos += ks1 - ks0;
+            if (ks0 == 0 && ks1 == p.n_ks) {
+                gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
+            } else {
+                const int slot = first_seg ? 0 : 1;
+                store_acc<NT>(red + (warp * 2 + slot) * kSlot + lane, acc, false);
+                if (lane == 0) seg_unit[warp][slot] = unit;
+            }
         }
-        for (; s < ks1; ++s) {
-            uint4 a1[kTPW];
-            uint2 b[NT];
-#pragma unroll
-            for (int it = 0; it < kTPW; ++it) a1[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) b[nt] = ldg_act(Bp + (s * 2 + nt) * 32);
-#pragma unroll
-            for (int it = 0; it < kTPW; ++it)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], b[nt]);
-        }
-        const bool first_seg = pos == wlo;
-        pos += ks1 - ks0;
-        if (ks0 == 0 && ks1 == p.n_ks) {
-            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
-        } else {
-            const int slot = first_seg ? 0 : 1;
-            store_acc<NT>(red + (warp * 2 + slot) * kSlot + lane, acc, false);
-            if (lane == 0) seg_unit[warp][slot] = unit;
-        }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // ---- CTA-level reduction of split super-tiles (owner = first contributor)
-    for (int slot = 0; slot < 2; ++slot) {
-        const long long unit = seg_unit[warp][slot];
-        if (unit < 0) continue;
-        bool owner = true;
-        for (int w = 0; w < warp && owner; ++w) owner = seg_unit[w][0] != unit && seg_unit[w][1] != unit;
-        if (!owner) continue;
-        zero_acc<NT>(acc);
-        add_acc<NT>(acc, red + (warp * 2 + slot) * kSlot + lane, false);
-        for (int w = warp + 1; w < kGemvWarps; ++w)
-            for (int s2 = 0; s2 < 2; ++s2)
-                if (seg_unit[w][s2] == unit) add_acc<NT>(acc, red + (w * 2 + s2) * kSlot + lane, false);
-        const long long ustart = unit * p.n_ks, uend = ustart + p.n_ks;
-        const int bl = (int)(unit / p.n_st);
-        const int st = (int)(unit - (long long)bl * p.n_st);
-        if (ustart >= clo && uend <= chi) {
-            gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
-            continue;
+        // ---- piece-level reduction of split super-tiles (owner = first contributor)
+        for (int slot = 0; slot < 2; ++slot) {
+            const long long unit = seg_unit[warp][slot];
+            if (unit < 0) continue;
+            bool owner = true;
+            for (int w = 0; w < warp && owner; ++w) owner = seg_unit[w][0] != unit && seg_unit[w][1] != unit;
+            if (!owner) continue;
+            zero_acc<NT>(acc);
+            add_acc<NT>(acc, red + (warp * 2 + slot) * kSlot + lane, false);
+            for (int w = warp + 1; w < kGemvWarps; ++w)
+                for (int s2 = 0; s2 < 2; ++s2)
+                    if (seg_unit[w][s2] == unit) add_acc<NT>(acc, red + (w * 2 + s2) * kSlot + lane, false);
+            const long long ustart = unit * p.n_ks, uend = ustart + p.n_ks;
+            const int bl = (int)(unit / p.n_st);
+            const int st = (int)(unit - (long long)bl * p.n_st);
+            if (ustart >= clo && uend <= chi) {
+                gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
+                continue;
+            }
+            // crosses a piece boundary: store the piece partial now, count the
+            // arrival after the CTA's last item (one fence for all of them)
+            const int first = owner_of(ustart - base, per_block, P);
+            const int last = owner_of(uend - 1 - base, per_block, P);
+            const int gslot = (q == first) ? 1 : 0;
+            store_acc<NT>(p.partial + (((long long)b * P + q) * 2 + gslot) * kSlot + lane, acc, true);
+            if (lane == 0) {
+                const int i = atomicAdd(&n_pend, 1);
+                if (i < kMaxPend) pend[i] = make_int4((int)unit, b, first, last);
+            }
         }
-        // crosses a CTA boundary: publish the CTA partial; last CTA reduces
-        const int first = owner_of(ustart, total, NC);
-        const int last = owner_of(uend - 1, total, NC);
-        const int gslot = (c == first) ? 1 : 0;
-        store_acc<NT>(p.partial + ((long long)c * 2 + gslot) * kSlot + lane, acc, true);
-        __threadfence();
+        __syncthreads();  // red[] / seg_unit reused by the next item
+    }
+    // ---- cross-piece reductions: every piece partial of this CTA is stored;
+    //      one fence, then the arrivals; the last arriving piece of a
+    //      super-tile sums the piece partials in piece order
+    __threadfence();
+    __syncthreads();
+    const int np = n_pend < kMaxPend ? n_pend : kMaxPend;
+    for (int e = warp; e < np; e += kGemvWarps) {
+        const int4 pe = pend[e];
+        const long long unit = pe.x;
+        const int b = pe.y, first = pe.z, last = pe.w;
         int prev = 0;
         if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
         prev = __shfl_sync(0xffffffffu, prev, 0);
@@ -507,8 +549,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         __threadfence();
         zero_acc<NT>(acc);
         for (int j = first; j <= last; ++j)
-            add_acc<NT>(acc, p.partial + ((long long)j * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
+            add_acc<NT>(acc, p.partial + (((long long)b * P + j) * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
         if (lane == 0) p.counters[unit] = 0;
+        const int bl = (int)(unit / p.n_st);
+        const int st = (int)(unit - (long long)bl * p.n_st);
         gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
     }
 }

@@ -138,3 +138,65 @@ def test_k_trace_matches_reference_controller(tiny, seed):
         assert np.array_equal(tag_ref, tel[:, 7].astype(np.int32)), which
     # the controller actually explored: probes, tests and sets all occur
     assert set(tel[:, 7].astype(int)) == {0, 1, 2}
+
+
+@pytest.mark.parametrize("p", [0.0, 0.7, 1.0])
+def test_replay_drafter_acceptance_and_lossless(tiny, p):
+    """Replay drafter (the model's own greedy continuation, each proposal
+    kept with probability p): the decode stays bitwise lossless, p=1 accepts every
+    draft, p=0 none, and the accepted prefixes follow the reference's
+    i.i.d. acceptance model (workload.hpp:80-86) within sampling error."""
+    shape, m, s = tiny
+    s.set_batch_invariant(True)
+    prompt = np.random.default_rng(7).integers(0, shape.vocab, 32).astype(np.int32)
+    truth, _, _ = s.decode(prompt, cb.decode_cfg(policy=0, max_new=220), telemetry_cap=0)
+    K = 4
+    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=K, max_new=200, replay=(truth, p, 99)), telemetry_cap=4096)
+    assert list(toks[:200]) == list(truth[:200])
+    spec = tel[tel[:, 1] == K]
+    emitted = spec[:, 2]
+    if p == 1.0:
+        assert np.all(emitted == K + 1)
+    elif p == 0.0:
+        assert np.all(emitted == 1)
+    else:
+        expect = sum(p ** j for j in range(K + 1))  # E[emitted] = sum_{j=0..K} p^j
+        assert abs(emitted.mean() - expect) < 0.5, (emitted.mean(), expect)
+
+
+def test_controller_speculates_when_drafts_are_good(tiny):
+    """With near-perfect drafts the utility controller leaves K=0 and the
+    effective tokens per iteration rise above 1 (device-measured costs)."""
+    shape, m, s = tiny
+    s.set_batch_invariant(True)
+    prompt = np.random.default_rng(8).integers(0, shape.vocab, 32).astype(np.int32)
+    truth, _, _ = s.decode(prompt, cb.decode_cfg(policy=0, max_new=420), telemetry_cap=0)
+    toks, tel, n_it = s.decode(prompt, cb.decode_cfg(policy=-1, max_new=400, k_max=7, replay=(truth, 0.95, 5)),
+                               telemetry_cap=4096)
+    assert list(toks[:400]) == list(truth[:400])
+    assert len(toks) / n_it > 1.5
+    assert (tel[:, 1] > 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("K", [1, 4, 8, 15])
+def test_step_is_batch_invariant(tiny, K):
+    """The logits of the pending token are bitwise identical whether it is
+    verified alone (K=0) or with K drafts riding along: every reduction is
+    cut at fixed, shape-determined points (expert GEMV pieces per block,
+    cluster split-K, 64-key attention chunks on absolute positions, one
+    combine expression), which is what makes greedy speculative decoding
+    bitwise lossless on the device."""
+    shape, m, _ = tiny
+    rng = np.random.default_rng(K)
+    prompt = rng.integers(0, shape.vocab, 70).astype(np.int32)
+    drafts = rng.integers(0, shape.vocab, K).astype(np.int32)
+    rows = []
+    for k in (0, K):
+        s = cb.Session(m, max_ctx=256, k_max=15)
+        s.set_batch_invariant(True)
+        s.enable_taps(True)
+        s.prefill(prompt)
+        s.verify(drafts[:k])
+        rows.append(s.tap("final_logits")[0].copy())
+        s.close()
+    assert np.array_equal(rows[0], rows[1])
