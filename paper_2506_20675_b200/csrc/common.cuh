@@ -92,7 +92,11 @@ __device__ __forceinline__ void trace_start(unsigned long long* slot) {
     if (slot != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *slot = globaltimer_raw();
     if (threadIdx.x == 0) {
         unsigned long long* c = cta_trace_slot(slot);
-        if (c != nullptr) c[0] = globaltimer_raw();
+        if (c != nullptr) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            c[0] = (globaltimer_raw() & ~0xFFull) | (smid & 0xFF);  // low byte: SM id (timer resolution >= 256 ns... ~32 ns)
+        }
     }
 }
 
