@@ -300,7 +300,7 @@ class Model:
         self.seed = seed
         self._g = shape.to_c()
         h = ctypes.c_void_p()
-        if ep_size == 1:
+        if ep_size == 1 and nccl_id is None:
             _check(lib().cascade_model_create(ctypes.byref(self._g), seed, device, ctypes.byref(h)))
         else:
             idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None

@@ -367,7 +367,7 @@ static int model_create(const cascade_geometry* g, uint64_t seed, int device, in
         set_err(CASCADE_ECUDA, std::string("weight init: ") + cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
     }
-    if (ep_size > 1) {
+    if (ep_size > 1 || uid) {  // an expert-parallel model (any world size, 1 included) owns a communicator
         if ((rc = nccl_load())) return fail(rc);
         if (!uid) {
             set_err(CASCADE_EINVAL, "nccl_unique_id is NULL for ep_size > 1");
@@ -1153,7 +1153,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         CK(launch_gemv(EPI_DOWN, dn, s->gemv_grid, st));
         PE();
         ++nk;
-        if (m->ep_size > 1) {
+        if (m->comm) {
             PB(11);
             const int nr = g_nccl.AllReduce(s->ycontrib, s->ycontrib, (size_t)T * (D.k + D.S) * D.d, kNcclFloat32,
                                             kNcclSum, m->comm, st);
@@ -1185,7 +1185,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         c.pf_bytes = (pf && l + 1 < D.L) ? D.wqkv_vec * 16 : 0;
         c.trace = tr(8);
         PB(8);
-        CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRowThreads), 0, st, m->ep_size == 1, c));
+        CK(launch_k(moe_combine_kernel, dim3(T), dim3(kRowThreads), 0, st, m->comm == nullptr, c));
         PE();
         ++nk;
     }

@@ -280,3 +280,25 @@ def test_utility_and_cost_breakdown(tiny):
     assert o.utility == pytest.approx(o.emitted * 1.0e6 / o.total, rel=1e-12)
     assert shape.top_k <= o.active_experts_per_layer <= shape.experts_per_layer
     s.close()
+
+
+def test_expert_parallel_single_rank_nccl_in_graph(tiny):
+    """The expert-parallel build (cascade_model_create_ep) on one rank: the
+    captured step graph carries the per-layer ncclAllReduce of the expert
+    outputs; with one rank it must reproduce the non-EP logits bitwise
+    (adding exact zeros / a single contribution is exact)."""
+    shape, m, _ = tiny
+    uid = cb.ep_unique_id()
+    mep = cb.Model(shape, cb.TINY_SEED, device=0, ep_rank=0, ep_size=1, nccl_id=uid)
+    rng = np.random.default_rng(3)
+    prompt = rng.integers(0, shape.vocab, 40).astype(np.int32)
+    drafts = rng.integers(0, shape.vocab, 5).astype(np.int32)
+    outs = []
+    for model in (m, mep):
+        s = cb.Session(model, max_ctx=256, k_max=8)
+        s.prefill(prompt)
+        o = s.verify(drafts)
+        outs.append((list(o.argmax[:6]), o.accepted, list(s.union_sizes())))
+        s.close()
+    mep.close()
+    assert outs[0] == outs[1]
