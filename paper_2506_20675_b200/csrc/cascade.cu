@@ -621,6 +621,8 @@ struct cascade_session {
     int invariant = 0;     // batch-invariant expert GEMV split (bitwise-lossless speculation)
     int* attn_arrive = nullptr;
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
+    int pf_o = 0;          // attention CTAs (the whole grid) bulk-prefetch W_o into L2 after their wait
+    int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
     int o_cluster = 0;     // same for the O projection
     uint16_t* kc = nullptr;
@@ -738,6 +740,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     // (the issuing kernels stall on the bulk-prefetch queue); off by default.
     s->prefetch = false;
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
+    if (const char* v = getenv("CASCADE_PF_O")) s->pf_o = v[0] == '1';
+    if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = v[0] == '1';
     if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = v[0] == '1';
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
@@ -861,6 +865,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.counters = s->ucounters;
     p.no_prologue = !s->umma_prologue;
     p.ring_stages = s->cluster_stages;
+    p.pf_self = s->pf_self;
     return p;
 }
 
@@ -989,8 +994,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ap.max_ctx = s->max_ctx;
         ap.max_chunks = s->max_chunks;
         ap.scale = 1.0f / sqrtf((float)D.hd);
-        ap.pf = pf ? w.wo : nullptr;
-        ap.pf_bytes = pf ? D.wo_vec * 16 : 0;
+        ap.pf = (pf || s->pf_o) ? w.wo : nullptr;
+        ap.pf_bytes = (pf || s->pf_o) ? D.wo_vec * 16 : 0;
         ap.trace = tr(2);
         // smem sized for this T's query rows; as many CTAs per SM as fit the
         // carveout (items are (chunk, kv head): 272 for OLMoE at ctx 1024)

@@ -117,6 +117,7 @@ struct UGemvParams {
     unsigned long long* dbg;   // optional phase stamps (scripts/umma_probe.cu)
     int no_prologue;           // A/B: issue nothing before griddepcontrol.wait
     int ring_stages;           // dense_gemv_cluster_kernel: ring depth (<= kCMaxStages)
+    int pf_self;               // dense_gemv_cluster_kernel: L2-prefetch the k-range beyond the ring before the wait
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -615,6 +616,15 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
                 mb_expect_tx(&full_bar[i], (uint32_t)n * (kUKsA + kUKsB));
                 bulk_g2s(ring + (size_t)i * kUStageBytes, a_base + (long long)(ks_lo + i * kUStageKs) * (kUKsA / 2),
                          (uint32_t)n * kUKsA, &full_bar[i], pol_a);
+            }
+            if (p.pf_self) {
+                // the rest of this CTA's weights -> L2 while the latency-bound predecessor runs
+                const char* src = reinterpret_cast<const char*>(a_base + (long long)(ks_lo + n_pre * kUStageKs) * (kUKsA / 2));
+                const long long bytes = (long long)(ks_hi - (ks_lo + n_pre * kUStageKs)) * kUKsA;
+                for (long long off = 0; off < bytes; off += 32768) {
+                    const uint32_t sz = (uint32_t)(bytes - off < 32768 ? bytes - off : 32768);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"(sz) : "memory");
+                }
             }
         }
         griddep_wait();
