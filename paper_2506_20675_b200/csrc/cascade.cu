@@ -1006,9 +1006,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         const int agrid = m->num_sms * per_sm;
         // fused combine needs [R][chunks] + [R] floats of the kernel's smem
         // and is only worth it while one CTA can keep every load in flight
-        // (<= 2 (row, 4-dim) items per thread); wider T use attn_combine
+        // (one (row, 4-dim) item per thread); wider T use attn_combine
         const bool fused = s->attn_fused && ((long long)(G * T) * (2 * s->max_chunks + 1)) * 4 <= asm_ &&
-                           G * T * (D.hd / 4) <= 2 * kAttnThreads;
+                           G * T * (D.hd / 4) <= kAttnThreads;
         ap.fused = fused;
         ap.arrive = s->attn_arrive;
         ap.out_bfrag = s->attn_out;

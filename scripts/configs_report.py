@@ -125,6 +125,7 @@ def main():
     report["config4_qwen15_latency"] = latency_sweep(cb.preset("qwen15"), prompts=2)
     report["config2_mixtral_latency_batch_invariant"] = latency_sweep(cb.preset("mixtral"), prompts=1,
                                                                        invariant=True)
+    report["config2_mixtral_ctx4096"] = latency_sweep(cb.preset("mixtral"), ctx=4096, prompts=1)
     report["config5_mixtral8x22b_24layer_slice"] = latency_sweep(cb.preset("mixtral8x22b").with_layers(24), prompts=1)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     path = os.path.join(ROOT, "gpurun_out", f"configs_{TAG}.json")
