@@ -272,6 +272,37 @@ CASCADE_API int cascade_decode(cascade_session* s, const int32_t* prompt, int n_
                    const cascade_decode_cfg* cfg, int32_t* out_tokens, int32_t* n_out,
                    double* telemetry, int32_t telemetry_cap, int32_t* n_iters);
 
+/* One cell of the reference scenario sweep (engine.hpp run_cell) on the
+ * device: the task's request stream (profile mix with cyclic acceptance
+ * phases and output lengths, token budget) decoded under one policy with
+ * the profile-driven replay drafter (proposals = the model's own greedy
+ * continuation, kept with the current phase's acceptance probability).
+ * Sets the session batch-invariant. */
+#define CASCADE_CELL_MAX_PROFILES 4
+#define CASCADE_CELL_MAX_PHASES 4
+typedef struct cascade_cell_cfg {
+    int32_t policy;            /* -1 adaptive, 0 none, else static K */
+    int32_t t_trial, max_trials, s_set, s_cap, k_max, k_start;   /* ControllerConfig */
+    double convergence_band;
+    int32_t baseline_refresh_interval, baseline_probe_len, backoff_enabled;
+    int32_t n_profiles;
+    double share[CASCADE_CELL_MAX_PROFILES];
+    int32_t n_phases[CASCADE_CELL_MAX_PROFILES];
+    double accept_p[CASCADE_CELL_MAX_PROFILES][CASCADE_CELL_MAX_PHASES];
+    double mean_duration[CASCADE_CELL_MAX_PROFILES][CASCADE_CELL_MAX_PHASES];
+    int32_t out_len_lo[CASCADE_CELL_MAX_PROFILES], out_len_hi[CASCADE_CELL_MAX_PROFILES];
+    int64_t tokens_per_cell;
+    int32_t prompt_len;
+    uint64_t seed;
+} cascade_cell_cfg;
+
+typedef struct cascade_cell_result {
+    int64_t requests, iterations, tokens;
+    double total_time, t_base, tpot, etr, cost, utility, utility_hmean;  /* device ns; engine.hpp CellResult */
+} cascade_cell_result;
+
+CASCADE_API int cascade_run_cell(cascade_session* s, const cascade_cell_cfg* cfg, cascade_cell_result* out);
+
 /* Library build identity: "sm_100a" plus the git hash baked at build. */
 CASCADE_API const char* cascade_build_info(void);
 

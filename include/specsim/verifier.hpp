@@ -217,4 +217,97 @@ inline RequestMetrics run_request(Verifier& verifier, Drafter& drafter, const Po
     return detail::finalize_metrics(analyzer, std::move(telemetry));
 }
 
+// Replay drafter driven by a reference WorkloadProfile: the keep
+// probability of each iteration's proposals is the current phase's
+// per_token_accept_prob, and the phase walker advances once per iteration,
+// exactly as the reference request loop does with ProfileState
+// (engine.hpp:122,159,176).
+class ProfileReplayDrafter {
+public:
+    ProfileReplayDrafter(std::vector<int32_t> truth, int n_prompt, const WorkloadProfile& profile, int vocab,
+                         uint64_t seed)
+        : truth_(std::move(truth)), n_prompt_(n_prompt), vocab_(vocab), rng_(seed), state_(profile, rng_) {
+        if (vocab < 2) throw std::invalid_argument("ProfileReplayDrafter: vocab must be >= 2");
+    }
+
+    std::vector<int32_t> propose(const std::vector<int32_t>& ctx, int k) {
+        std::vector<int32_t> out;
+        const double p = state_.phase().per_token_accept_prob;
+        const long pos = static_cast<long>(ctx.size()) - n_prompt_;
+        std::uniform_real_distribution<double> u(0.0, 1.0);
+        for (int i = 0; i < k; ++i) {
+            const long j = pos + i;
+            if (j < 0 || j >= static_cast<long>(truth_.size())) break;
+            int32_t t = truth_[j];
+            if (u(rng_) >= p) t = static_cast<int32_t>((t + 1) % vocab_);
+            out.push_back(t);
+        }
+        state_.advance(rng_);
+        return out;
+    }
+
+private:
+    std::vector<int32_t> truth_;
+    int n_prompt_;
+    int vocab_;
+    Rng rng_;
+    ProfileState state_;
+};
+
+// K=0 stand-in drafter (proposes nothing).
+struct NoDrafter {
+    std::vector<int32_t> propose(const std::vector<int32_t>&, int) const { return {}; }
+};
+
+// One cell of the reference scenario sweep (engine.hpp run_cell / run_scenario,
+// 300-466) on the device: the task's request stream (profile mix, output
+// lengths, token budget) is drawn with the reference's policy-independent
+// seeds, every request gets a random prompt, its greedy continuation is
+// recorded with a K=0 decode, and the request is then decoded under the
+// policy with the profile-driven replay drafter.  Costs are the device's;
+// the aggregation is the reference's (tpot, ETR, cost, utility, harmonic mean).
+// The session must be batch-invariant so replayed drafts stay aligned.
+inline CellResult run_cell(Verifier& verifier, int vocab, const RequestStream& task, const Policy& policy,
+                           long tokens_per_cell, int prompt_len, uint64_t seed, const GpuRunOptions& opt = {}) {
+    if (prompt_len < 1) throw std::invalid_argument("run_cell: prompt_len must be >= 1");
+    CellResult cell;
+    cell.policy = policy.label();
+    const std::uint64_t wseed = splitmix64(seed);
+    Rng stream_rng(wseed);
+    RequestStream stream = task;
+    stream.max_tokens = tokens_per_cell;
+    StreamSampler sampler(stream);
+    std::vector<double> utils;
+    double t_base_sum = 0.0;
+    while (!sampler.exhausted()) {
+        const auto [profile, len] = sampler.next_request(stream_rng);
+        Rng prng(splitmix64(wseed + 0x9E3779B97F4A7C15ull * static_cast<std::uint64_t>(cell.requests + 1)));
+        std::vector<int32_t> prompt(static_cast<std::size_t>(prompt_len));
+        std::uniform_int_distribution<int32_t> tok(0, vocab - 1);
+        for (int32_t& t : prompt) t = tok(prng);
+        std::vector<int32_t> truth_toks = prompt;
+        NoDrafter none_drafter;
+        check_status(cascade_session_reset(verifier.session()));
+        run_request(verifier, none_drafter, Policy::none(), truth_toks, len + CASCADE_MAX_TOKENS, opt);
+        std::vector<int32_t> truth(truth_toks.begin() + prompt_len, truth_toks.end());
+        ProfileReplayDrafter drafter(std::move(truth), prompt_len, *profile, vocab, prng());
+        std::vector<int32_t> toks = prompt;
+        check_status(cascade_session_reset(verifier.session()));
+        RequestMetrics m = run_request(verifier, drafter, policy, toks, len, opt);
+        ++cell.requests;
+        cell.iterations += m.iterations;
+        cell.tokens += m.tokens;
+        cell.total_time += m.total_time;
+        t_base_sum += m.t_base;
+        utils.push_back(m.utility);
+    }
+    cell.t_base = t_base_sum / static_cast<double>(cell.requests);
+    cell.tpot = cell.total_time / static_cast<double>(cell.tokens);
+    cell.etr = static_cast<double>(cell.tokens) / static_cast<double>(cell.iterations);
+    cell.cost = (cell.total_time / static_cast<double>(cell.iterations)) / cell.t_base;
+    cell.utility = cell.etr / cell.cost;
+    cell.utility_hmean = harmonic_mean(utils);
+    return cell;
+}
+
 }  // namespace specsim

@@ -116,6 +116,37 @@ class DecodeCfg(ctypes.Structure):
     ]
 
 
+class CellCfg(ctypes.Structure):
+    _fields_ = [
+        ("policy", ctypes.c_int32),
+        ("t_trial", ctypes.c_int32),
+        ("max_trials", ctypes.c_int32),
+        ("s_set", ctypes.c_int32),
+        ("s_cap", ctypes.c_int32),
+        ("k_max", ctypes.c_int32),
+        ("k_start", ctypes.c_int32),
+        ("convergence_band", ctypes.c_double),
+        ("baseline_refresh_interval", ctypes.c_int32),
+        ("baseline_probe_len", ctypes.c_int32),
+        ("backoff_enabled", ctypes.c_int32),
+        ("n_profiles", ctypes.c_int32),
+        ("share", ctypes.c_double * 4),
+        ("n_phases", ctypes.c_int32 * 4),
+        ("accept_p", (ctypes.c_double * 4) * 4),
+        ("mean_duration", (ctypes.c_double * 4) * 4),
+        ("out_len_lo", ctypes.c_int32 * 4),
+        ("out_len_hi", ctypes.c_int32 * 4),
+        ("tokens_per_cell", ctypes.c_int64),
+        ("prompt_len", ctypes.c_int32),
+        ("seed", ctypes.c_uint64),
+    ]
+
+
+class CellResult(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("requests", "iterations", "tokens")] + \
+        [(n, ctypes.c_double) for n in ("total_time", "t_base", "tpot", "etr", "cost", "utility", "utility_hmean")]
+
+
 # ----------------------------------------------------------------- geometry presets
 @dataclass
 class ModelShape:
@@ -245,6 +276,7 @@ def lib() -> ctypes.CDLL:
         ),
         "cascade_enable_taps": (ctypes.c_int, [P, ctypes.c_int]),
         "cascade_set_batch_invariant": (ctypes.c_int, [P, ctypes.c_int]),
+        "cascade_run_cell": (ctypes.c_int, [P, ctypes.POINTER(CellCfg), ctypes.POINTER(CellResult)]),
         "cascade_read_tap": (ctypes.c_int, [P, ctypes.c_int, P, szt]),
         "cascade_read_weight": (
             ctypes.c_int,
@@ -448,6 +480,31 @@ class Session:
                                             _i32p(kind), cap, ctypes.byref(n)))
         return out[: n.value], kind[: n.value]
 
+    def run_cell(self, policy: int, profiles, tokens_per_cell: int = 512, prompt_len: int = 64, seed: int = 1,
+                 **controller) -> dict:
+        """One reference scenario cell on the device (cascade_run_cell).  `profiles` is a list of
+        (share, [(accept_p, mean_duration), ...], (out_len_lo, out_len_hi)); policy -1 adaptive,
+        0 none, else static K."""
+        c = CellCfg()
+        d = decode_cfg(policy=policy, **controller)
+        for name in ("policy", "t_trial", "max_trials", "s_set", "s_cap", "k_max", "k_start", "convergence_band",
+                     "baseline_refresh_interval", "baseline_probe_len", "backoff_enabled"):
+            setattr(c, name, getattr(d, name))
+        c.n_profiles = len(profiles)
+        for i, (share, phases, (lo, hi)) in enumerate(profiles):
+            c.share[i] = share
+            c.n_phases[i] = len(phases)
+            for j, (pa, dur) in enumerate(phases):
+                c.accept_p[i][j] = pa
+                c.mean_duration[i][j] = dur
+            c.out_len_lo[i], c.out_len_hi[i] = lo, hi
+        c.tokens_per_cell = tokens_per_cell
+        c.prompt_len = prompt_len
+        c.seed = seed
+        r = CellResult()
+        _check(lib().cascade_run_cell(self.h, ctypes.byref(c), ctypes.byref(r)))
+        return {n: getattr(r, n) for n, _ in CellResult._fields_}
+
     def set_batch_invariant(self, on: bool = True):
         """Fixed expert-GEMV pieces: bitwise batch-invariant logits (lossless speculation)."""
         _check(lib().cascade_set_batch_invariant(self.h, 1 if on else 0))
@@ -515,3 +572,33 @@ def decode_cfg(policy: int = -1, max_new: int = 128, ngram_n: int = 3, **control
         c.replay_p = float(p)
         c.replay_seed = int(seed)
     return c
+
+
+def run_scenario(session: "Session", tasks: dict, policies: list, tokens_per_cell: int = 512, **kw) -> dict:
+    """The reference scenario sweep (engine.hpp run_scenario + compare_policies) over
+    verifier-backed cells: every (task, policy) cell runs on the device; speedup =
+    tpot(none) / tpot(policy) per task; OLS regression of speedup on utility."""
+    cells = []
+    for tname, profiles in tasks.items():
+        for pol in policies:
+            r = session.run_cell(pol, profiles, tokens_per_cell=tokens_per_cell, **kw)
+            r.update(task=tname, policy=("none" if pol == 0 else "adaptive" if pol < 0 else f"static:{pol}"))
+            cells.append(r)
+    base = {c["task"]: c for c in cells if c["policy"] == "none"}
+    pts = []
+    for c in cells:
+        c["speedup"] = base[c["task"]]["tpot"] / c["tpot"] if c["task"] in base else None
+        if c["speedup"] is not None:
+            pts.append((c["utility"], c["speedup"]))
+    reg = None
+    if len(pts) >= 2:
+        x = np.array([p[0] for p in pts])
+        y = np.array([p[1] for p in pts])
+        sxx = float(((x - x.mean()) ** 2).sum())
+        if sxx > 0:
+            slope = float(((x - x.mean()) * (y - y.mean())).sum() / sxx)
+            icpt = float(y.mean() - slope * x.mean())
+            syy = float(((y - y.mean()) ** 2).sum())
+            r2 = 1.0 if syy == 0 else float(((x - x.mean()) * (y - y.mean())).sum() ** 2 / (sxx * syy))
+            reg = {"slope": slope, "intercept": icpt, "r2": r2, "n": len(pts)}
+    return {"cells": cells, "utility_speedup": reg}

@@ -108,3 +108,75 @@ extern "C" int cascade_decode(cascade_session* s, const int32_t* prompt, int n_p
         return cascade_internal_set_error(CASCADE_ERUNTIME, e.what());
     }
 }
+
+extern "C" int cascade_run_cell(cascade_session* s, const cascade_cell_cfg* cfg, cascade_cell_result* out) {
+    using namespace specsim;
+    if (!s || !cfg || !out) return cascade_internal_set_error(CASCADE_EINVAL, "cascade_run_cell: NULL argument");
+    try {
+        if (cfg->n_profiles < 1 || cfg->n_profiles > CASCADE_CELL_MAX_PROFILES)
+            throw std::invalid_argument("cascade_run_cell: n_profiles must be in [1,4]");
+        Policy policy;
+        if (cfg->policy < 0) {
+            ControllerConfig c;
+            c.t_trial = cfg->t_trial;
+            c.max_trials = cfg->max_trials;
+            c.s_set = cfg->s_set;
+            c.s_cap = cfg->s_cap;
+            c.k_max = cfg->k_max;
+            c.k_start = cfg->k_start;
+            c.convergence_band = cfg->convergence_band;
+            c.baseline_refresh_interval = cfg->baseline_refresh_interval;
+            c.baseline_probe_len = cfg->baseline_probe_len;
+            c.backoff_enabled = cfg->backoff_enabled != 0;
+            policy = Policy::adaptive(c);
+        } else if (cfg->policy == 0) {
+            policy = Policy::none();
+        } else {
+            if (cfg->policy > CASCADE_MAX_K) throw std::invalid_argument("static policy: k must be in [0,15]");
+            policy.kind = Policy::Kind::static_k;
+            policy.k = cfg->policy;
+        }
+        RequestStream task;
+        for (int i = 0; i < cfg->n_profiles; ++i) {
+            if (cfg->n_phases[i] < 1 || cfg->n_phases[i] > CASCADE_CELL_MAX_PHASES)
+                throw std::invalid_argument("cascade_run_cell: n_phases must be in [1,4]");
+            WorkloadProfile prof;
+            prof.name = "profile" + std::to_string(i);
+            for (int j = 0; j < cfg->n_phases[i]; ++j) {
+                AcceptancePhase ph;
+                ph.per_token_accept_prob = cfg->accept_p[i][j];
+                ph.mean_duration = cfg->mean_duration[i][j];
+                prof.phases.push_back(ph);
+            }
+            prof.transition = PhaseTransition::cyclic;
+            prof.output_len.lo = cfg->out_len_lo[i];
+            prof.output_len.hi = cfg->out_len_hi[i];
+            task.mix.emplace_back(prof, cfg->share[i]);
+        }
+        task.max_tokens = cfg->tokens_per_cell;
+        int rc = cascade_set_batch_invariant(s, 1);
+        if (rc) return rc;
+        GpuRunOptions opt;
+        opt.k_limit = CASCADE_MAX_K;
+        Verifier v(s);
+        const CellResult c = run_cell(v, cascade_internal_vocab(s), task, policy, cfg->tokens_per_cell,
+                                      cfg->prompt_len, cfg->seed, opt);
+        out->requests = c.requests;
+        out->iterations = c.iterations;
+        out->tokens = c.tokens;
+        out->total_time = c.total_time;
+        out->t_base = c.t_base;
+        out->tpot = c.tpot;
+        out->etr = c.etr;
+        out->cost = c.cost;
+        out->utility = c.utility;
+        out->utility_hmean = c.utility_hmean;
+        return CASCADE_OK;
+    } catch (const std::invalid_argument& e) {
+        return cascade_internal_set_error(CASCADE_EINVAL, e.what());
+    } catch (const MissingBaselineError& e) {
+        return cascade_internal_set_error(CASCADE_ENOBASE, e.what());
+    } catch (const std::exception& e) {
+        return cascade_internal_set_error(CASCADE_ERUNTIME, e.what());
+    }
+}

@@ -116,6 +116,25 @@ def spec_decode(shape, seed=3, max_new=256, ps=(0.6, 0.8, 0.95), statics=(1, 2, 
     return res
 
 
+def scenario_sweep(shape, seed=5):
+    """Reference scenario sweep (engine.hpp run_scenario) with verifier-backed cells:
+    two tasks (a phased high/low-acceptance profile and a low-acceptance mix) x
+    {none, static 2, static 4, adaptive}; speedup vs none and utility->speedup OLS."""
+    m = cb.Model(shape, seed)
+    s = cb.Session(m, max_ctx=1024, k_max=15)
+    tasks = {"phased_0.9_0.5": [(1.0, [(0.9, 16.0), (0.5, 16.0)], (96, 128))],
+             "mix_0.3_0.6": [(0.5, [(0.3, 1.0)], (96, 96)), (0.5, [(0.6, 1.0)], (128, 128))]}
+    rep = cb.run_scenario(s, tasks, [0, 2, 4, -1], tokens_per_cell=512, prompt_len=64, seed=seed, k_max=7)
+    s.close()
+    m.close()
+    for c in rep["cells"]:
+        for k in ("total_time", "t_base", "tpot"):
+            c[k] = round(c[k], 1)
+        for k in ("etr", "cost", "utility", "utility_hmean", "speedup"):
+            c[k] = round(c[k], 4) if c[k] is not None else None
+    return rep
+
+
 def main():
     report = {"peak_hbm_gbs": PEAK}
     report["config3_olmoe"] = latency_sweep(cb.preset("olmoe"))
@@ -125,6 +144,7 @@ def main():
     report["config4_qwen15_latency"] = latency_sweep(cb.preset("qwen15"), prompts=2)
     report["config2_mixtral_latency_batch_invariant"] = latency_sweep(cb.preset("mixtral"), prompts=1,
                                                                        invariant=True)
+    report["config4_qwen15_scenario"] = scenario_sweep(cb.preset("qwen15"))
     report["config2_mixtral_ctx4096"] = latency_sweep(cb.preset("mixtral"), ctx=4096, prompts=1)
     report["config5_mixtral8x22b_24layer_slice"] = latency_sweep(cb.preset("mixtral8x22b").with_layers(24), prompts=1)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

@@ -200,3 +200,23 @@ def test_step_is_batch_invariant(tiny, K):
         rows.append(s.tap("final_logits")[0].copy())
         s.close()
     assert np.array_equal(rows[0], rows[1])
+
+
+def test_scenario_cells_on_device(tiny):
+    """The reference scenario sweep with verifier-backed cells: per-task
+    speedups against the `none` policy, the reference aggregation (Theorem 1:
+    utility * TPOT == t_base per cell) and a utility/speedup regression."""
+    shape, m, s = tiny
+    tasks = {"phased": [(1.0, [(0.9, 6.0), (0.4, 6.0)], (40, 60))],
+             "low": [(0.5, [(0.3, 1.0)], (40, 40)), (0.5, [(0.6, 1.0)], (50, 50))]}
+    rep = cb.run_scenario(s, tasks, [0, 2, -1], tokens_per_cell=160, prompt_len=24, seed=3, k_max=4)
+    cells = rep["cells"]
+    assert len(cells) == 6
+    for c in cells:
+        assert c["requests"] >= 2 and c["tokens"] >= 160
+        assert abs(c["utility"] * c["tpot"] - c["t_base"]) <= 1e-9 * c["t_base"]
+        if c["policy"] == "none":
+            assert c["speedup"] == 1.0 and c["etr"] == 1.0
+        else:
+            assert c["etr"] > 1.0
+    assert rep["utility_speedup"] is not None and rep["utility_speedup"]["n"] == 6
