@@ -511,6 +511,39 @@ static cudaError_t gemv_smem_attr() {
     return e;
 }
 
+// ---------------------------------------------------------------- SM rate calibration
+// Streaming rates differ by SM by a few percent, consistently (profiles:
+// scripts/sm_speed.py), and a static equal split waits for the slowest
+// SM.  At session creation every CTA of a 2-per-SM grid streams an equal
+// slice of the expert weights with the GEMV's load pattern; the per-SM
+// rates give the piece weights of the expert GEMVs' grid-wide split.
+__global__ void __launch_bounds__(kGemvThreads, 2) sm_rate_probe_kernel(const uint4* src, long long per_cta_vec,
+                                                                       unsigned long long* out) {
+    const uint64_t pol = policy_evict_first();
+    const uint4* base = src + (long long)blockIdx.x * per_cta_vec;
+    __syncthreads();
+    const unsigned long long t0 = globaltimer_raw();
+    uint32_t acc = 0;
+    for (long long i = threadIdx.x; i < per_cta_vec; i += (long long)blockDim.x * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long j = i + (long long)u * blockDim.x;
+            v[u] = j < per_cta_vec ? ldg_stream(base + j, pol) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+    }
+    __syncthreads();
+    const unsigned long long t1 = globaltimer_raw();
+    if (threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        out[blockIdx.x * 2] = smid | ((unsigned long long)(acc & 1u) << 40);  // acc keeps the loads alive
+        out[blockIdx.x * 2 + 1] = t1 - t0;
+    }
+}
+
 // Cluster size for the split-K dense GEMV over n_units 128-row units: the
 // largest C <= 8 with n_units * C <= SMs whose clusters can all be resident
 // at once (one wave); 0 = use the stream-K path.
@@ -619,6 +652,10 @@ struct cascade_session {
     int umma_prologue = 1;
     int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
     int invariant = 0;     // batch-invariant expert GEMV split (bitwise-lossless speculation)
+    int* sm_index = nullptr;   // %smid -> dense SM index (SM-weighted expert GEMV split), nullptr: off
+    int* sm_slot = nullptr;
+    int* sm_cum = nullptr;     // [gemv_grid + 1]
+    std::vector<float> sm_weight;  // per dense SM (host copy, diagnostics)
     int* attn_arrive = nullptr;
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
     int pf_o = 0;          // attention CTAs (the whole grid) bulk-prefetch W_o into L2 after their wait
@@ -657,6 +694,102 @@ extern "C" int cascade_session_destroy(cascade_session* s) {
     if (s->h_result) cudaFreeHost(s->h_result);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
     delete s;
+    return CASCADE_OK;
+}
+
+// SM-weighted split of the expert GEMVs (see sm_rate_probe_kernel).  Only
+// when the GEMV occupancy is exactly 2 CTAs per SM (the work index relies
+// on it) and the weights are large enough for a meaningful probe.
+static int calibrate_sm_rates(cascade_session* s) {
+    cascade_model* m = s->m;
+    const Dims D(m->g);
+    // measured: the CTA exit spread did not shrink and both expert GEMVs got
+    // 2-4% slower (profiles/r01d/ab_sm_weights.txt), so it is opt-in
+    const char* v = getenv("CASCADE_SM_WEIGHTS");
+    if (!v || v[0] != '1') return CASCADE_OK;
+    int occ1 = 0, occ2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, stream_gemv_kernel<1, EPI_GATEUP>, kGemvThreads,
+                                                      gemv_smem_bytes<1>()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, stream_gemv_kernel<2, EPI_DOWN>, kGemvThreads,
+                                                      gemv_smem_bytes<2>()) != cudaSuccess) {
+        cudaGetLastError();
+        return CASCADE_OK;
+    }
+    int occp = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occp, sm_rate_probe_kernel, kGemvThreads, 0);
+    if (occ1 != 2 || occ2 != 2 || occp < 2 || s->gemv_grid != 2 * m->num_sms || m->layers.empty()) return CASCADE_OK;
+    for (int t = 0; t < 5; ++t) {  // the other instantiations must be 2 per SM as well
+        const void* k[5] = {(const void*)stream_gemv_kernel<1, EPI_STORE>, (const void*)stream_gemv_kernel<1, EPI_DOWN>,
+                            (const void*)stream_gemv_kernel<2, EPI_GATEUP>, (const void*)stream_gemv_kernel<2, EPI_STORE>,
+                            (const void*)stream_gemv_kernel<1, EPI_ARGMAX>};
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k[t], kGemvThreads, t < 2 || t == 4 ? gemv_smem_bytes<1>() : gemv_smem_bytes<2>());
+        if (o != 2) return CASCADE_OK;
+    }
+    const int grid = s->gemv_grid;
+    const long long avail_vec = (long long)m->n_blocks * D.w13_vec;
+    long long per_cta = std::min<long long>(avail_vec / grid, (4ll << 20) / 16);
+    if (per_cta * 16 < (256 << 10)) return CASCADE_OK;  // too little to time
+    unsigned long long* d_out = nullptr;
+    if (cudaMalloc(&d_out, (size_t)grid * 2 * 8) != cudaSuccess) {
+        cudaGetLastError();
+        return CASCADE_OK;
+    }
+    std::vector<unsigned long long> h((size_t)grid * 2);
+    std::vector<double> dur(256, 0.0);
+    std::vector<int> cnt(256, 0);
+    const int reps = 7;
+    bool ok = true;
+    for (int r = 0; r < reps && ok; ++r) {
+        sm_rate_probe_kernel<<<grid, kGemvThreads, 0, s->stream>>>(m->layers[0].w13, per_cta, d_out);
+        ok = cudaStreamSynchronize(s->stream) == cudaSuccess &&
+             cudaMemcpy(h.data(), d_out, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess;
+        if (!ok || r == 0) continue;  // first run warms up
+        for (int b = 0; b < grid; ++b) {
+            const int smid = (int)(h[2 * b] & 0xFF);
+            dur[smid] += (double)h[2 * b + 1];
+            cnt[smid] += 1;
+        }
+    }
+    cudaFree(d_out);
+    if (!ok) {
+        cudaGetLastError();
+        return CASCADE_OK;
+    }
+    std::vector<int> index(256, -1);
+    std::vector<double> rate;
+    for (int smid = 0; smid < 256; ++smid) {
+        if (cnt[smid] == 0) continue;
+        if (cnt[smid] != 2 * (reps - 1)) return CASCADE_OK;  // not exactly 2 CTAs per SM: keep the equal split
+        index[smid] = (int)rate.size();
+        rate.push_back(cnt[smid] / dur[smid]);
+    }
+    if ((int)rate.size() * 2 != grid) return CASCADE_OK;
+    double mean = 0.0;
+    for (double r : rate) mean += r;
+    mean /= rate.size();
+    s->sm_weight.assign(rate.size(), 1.0f);
+    std::vector<double> w(grid);
+    for (size_t i = 0; i < rate.size(); ++i) {
+        const double wi = std::min(1.2, std::max(0.8, rate[i] / mean));
+        s->sm_weight[i] = (float)wi;
+        w[2 * i] = w[2 * i + 1] = std::round(wi * 256.0) / 256.0;  // quantised: a stable split for the session
+    }
+    double tot = 0.0;
+    for (double x : w) tot += x;
+    std::vector<int> cum(grid + 1);
+    double acc = 0.0;
+    for (int i = 0; i <= grid; ++i) {
+        cum[i] = (int)std::llround(acc / tot * (double)(1 << 24));
+        if (i < grid) acc += w[i];
+    }
+    cum[grid] = 1 << 24;
+    int rc;
+    if ((rc = salloc(s, &s->sm_index, 256 * 4)) || (rc = salloc(s, &s->sm_slot, 256 * 4)) ||
+        (rc = salloc(s, &s->sm_cum, (size_t)(grid + 1) * 4)))
+        return rc;
+    CK(cudaMemcpy(s->sm_index, index.data(), 256 * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(s->sm_cum, cum.data(), (size_t)(grid + 1) * 4, cudaMemcpyHostToDevice));
     return CASCADE_OK;
 }
 
@@ -789,6 +922,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
     }
+    if ((rc = calibrate_sm_rates(s))) return fail(rc);
     *out = s;
     return CASCADE_OK;
 }
@@ -876,6 +1010,9 @@ static GemvParams gemv_base(cascade_session* s, int T) {
     p.partial = s->partial;
     p.counters = s->counters;
     p.invariant = s->invariant;
+    p.sm_index = s->sm_index;
+    p.sm_slot = s->sm_slot;
+    p.cum = s->sm_cum;
     p.n_blocks = 1;
     p.l2_prologue = s->l2_prologue;
     p.trigger = s->gemv_trigger;

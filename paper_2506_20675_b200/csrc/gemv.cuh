@@ -71,6 +71,13 @@ struct GemvParams {
     int publish;
     int* union_size;           // out (publish): distinct routed experts of the step
     int invariant;             // 1: fixed pieces per block (batch-invariant sums); 0: stream-K over all blocks
+    // SM-speed-weighted pieces: streaming rates differ by SM (a fixed
+    // property of the part, +-3%; the slowest SM sets the kernel time), so
+    // the work index of a CTA is (dense SM index, slot on that SM) and the
+    // pieces of a grid-wide split are sized by the SM's measured rate.
+    const int* sm_index;       // %smid -> dense SM index (or -1), nullptr: work index = blockIdx.x
+    int* sm_slot;              // per-%smid arrival counters (parity = slot of the 2 CTAs of an SM)
+    const int* cum;            // [grid + 1] cumulative piece weights, cum[grid] = 1 << 24 (nullptr: equal)
 };
 
 constexpr int kGemvThreads = 256;
@@ -258,6 +265,40 @@ __device__ __forceinline__ int owner_of(long long q, long long total, int n) {
     return (int)(((q + 1) * n + total - 1) / total) - 1;
 }
 
+// piece boundaries of a split of [0, total) into n pieces: weighted by
+// cum (n == grid) or equal
+__device__ __forceinline__ long long piece_start(long long total, int q, int n, const int* cum) {
+    if (cum != nullptr && n == (int)gridDim.x) return (total * (long long)__ldg(cum + q)) >> 24;
+    return total * q / n;
+}
+__device__ __forceinline__ int piece_owner(long long pos, long long total, int n, const int* cum) {
+    if (cum == nullptr || n != (int)gridDim.x) return owner_of(pos, total, n);
+    int lo = 0, hi = n - 1;  // largest q with piece_start(q) <= pos
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (piece_start(total, mid, n, cum) <= pos) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Work index of this CTA: (dense SM index, slot) when the SM map is set.
+// Each SM hosts exactly 2 CTAs of a 2*SMs grid (register-limited), and each
+// launch adds 2 to the SM's counter, so its parity tells the two apart.
+__device__ __forceinline__ int gemv_work_index(const GemvParams& p) {
+    __shared__ int s_wi;
+    if (p.sm_index == nullptr) return (int)blockIdx.x;
+    if (threadIdx.x == 0) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const int dense = p.sm_index[smid];
+        const int slot = atomicAdd(p.sm_slot + smid, 1) & 1;
+        s_wi = dense * 2 + slot;
+    }
+    __syncthreads();
+    return s_wi;
+}
+
 template <int NT>
 __device__ __forceinline__ void zero_acc(float (&acc)[kTPW][NT][4]) {
 #pragma unroll
@@ -342,6 +383,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     uint4 a[kUnroll][kTPW];
     bool pre = false;
     const bool dense = !routed && p.list == nullptr && p.count == nullptr;
+    const int wi = gemv_work_index(p);
     if (routed && p.early_list) {
         // the router's top-k was written two kernels back (final): build the
         // union now so the prologue can address the first expert weights
@@ -360,9 +402,10 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
         const int nb0 = p.invariant ? U0 : (U0 > 0 ? 1 : 0);
         const int P0 = block_pieces(p, pb0);
         long long wlo0 = 0, whi0 = 0;
-        if ((int)blockIdx.x < nb0 * P0) {
-            const int b0 = (int)blockIdx.x / P0, q0 = (int)blockIdx.x - b0 * P0;
-            const long long clo0 = (long long)b0 * pb0 + pb0 * q0 / P0, chi0 = (long long)b0 * pb0 + pb0 * (q0 + 1) / P0;
+        if (wi < nb0 * P0) {
+            const int b0 = wi / P0, q0 = wi - b0 * P0;
+            const long long clo0 = (long long)b0 * pb0 + piece_start(pb0, q0, P0, p.cum);
+            const long long chi0 = (long long)b0 * pb0 + piece_start(pb0, q0 + 1, P0, p.cum);
             wlo0 = clo0 + (chi0 - clo0) * warp / kGemvWarps;
             whi0 = clo0 + (chi0 - clo0) * (warp + 1) / kGemvWarps;
         }
@@ -429,11 +472,11 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     __shared__ int n_pend;
     if (threadIdx.x == 0) n_pend = 0;
     __syncthreads();
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    for (int item = wi; item < n_items; item += gridDim.x) {
         const int b = item / P, q = item - b * P;
         // this piece of block b, in flat (unit, k-step) positions
         const long long base = (long long)b * per_block;
-        const long long clo = base + per_block * q / P, chi = base + per_block * (q + 1) / P;
+        const long long clo = base + piece_start(per_block, q, P, p.cum), chi = base + piece_start(per_block, q + 1, P, p.cum);
         const long long wlo = clo + (chi - clo) * warp / kGemvWarps;
         const long long whi = clo + (chi - clo) * (warp + 1) / kGemvWarps;
         if (lane == 0) {
@@ -521,8 +564,8 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
             }
             // crosses a piece boundary: store the piece partial now, count the
             // arrival after the CTA's last item (one fence for all of them)
-            const int first = owner_of(ustart - base, per_block, P);
-            const int last = owner_of(uend - 1 - base, per_block, P);
+            const int first = piece_owner(ustart - base, per_block, P, p.cum);
+            const int last = piece_owner(uend - 1 - base, per_block, P, p.cum);
             const int gslot = (q == first) ? 1 : 0;
             store_acc<NT>(p.partial + (((long long)b * P + q) * 2 + gslot) * kSlot + lane, acc, true);
             if (lane == 0) {
