@@ -23,7 +23,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcascade.so")
+LIB_PATH = os.environ.get("CASCADE_LIB_PATH") or os.path.join(_HERE, "libcascade.so")  # A/B builds only
 
 MAX_TOKENS = 16
 MAX_K = MAX_TOKENS - 1
