@@ -367,7 +367,10 @@ static int model_create(const cascade_geometry* g, uint64_t seed, int device, in
         set_err(CASCADE_ECUDA, std::string("weight init: ") + cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
     }
-    if (ep_size > 1 || uid) {  // an expert-parallel model (any world size, 1 included) owns a communicator
+    // CASCADE_EP_NOCOMM=1 (tests only): an expert shard without a communicator,
+    // so one GPU can run every shard of a world and check the partition
+    const char* nocomm = getenv("CASCADE_EP_NOCOMM");
+    if ((ep_size > 1 || uid) && !(nocomm && nocomm[0] == '1')) {  // an expert-parallel model (any world size, 1 included) owns a communicator
         if ((rc = nccl_load())) return fail(rc);
         if (!uid) {
             set_err(CASCADE_EINVAL, "nccl_unique_id is NULL for ep_size > 1");

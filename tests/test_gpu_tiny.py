@@ -302,3 +302,39 @@ def test_expert_parallel_single_rank_nccl_in_graph(tiny):
         s.close()
     mep.close()
     assert outs[0] == outs[1]
+
+
+def test_expert_shards_partition_the_moe_output(tiny, monkeypatch):
+    """Expert parallelism on one GPU: with CASCADE_EP_NOCOMM=1 each shard
+    model (rank r of G) runs without the all-reduce, so its layer-0 MoE
+    output is the sum over its own experts only (the others contribute exact
+    zeros).  The shards' outputs must add up to the full model's, and their
+    union sizes (the global distinct-expert count) must agree with it."""
+    shape, m, _ = tiny
+    monkeypatch.setenv("CASCADE_EP_NOCOMM", "1")
+    rng = np.random.default_rng(11)
+    prompt = rng.integers(0, shape.vocab, 30).astype(np.int32)
+    drafts = rng.integers(0, shape.vocab, 4).astype(np.int32)
+
+    def layer0_moe(model):
+        s = cb.Session(model, max_ctx=128, k_max=8)
+        s.enable_taps(True)
+        s.prefill(prompt)
+        s.verify(drafts)
+        out = s.tap("moe_out")[0, :5].copy()
+        us = list(s.union_sizes())
+        s.close()
+        return out, us
+
+    full, us_full = layer0_moe(m)
+    for G in (2, 4):
+        parts = []
+        for r in range(G):
+            mr = cb.Model(shape, cb.TINY_SEED, device=0, ep_rank=r, ep_size=G, nccl_id=bytes(128))
+            out, us = layer0_moe(mr)
+            mr.close()
+            assert us[0] == us_full[0]
+            parts.append(out)
+        total = np.sum(parts, axis=0)
+        assert np.allclose(total, full, rtol=1e-5, atol=1e-6), float(np.abs(total - full).max())
+        assert sum(np.abs(p).max() > 0 for p in parts) >= 2  # the work really is split across shards
