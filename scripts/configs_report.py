@@ -116,6 +116,42 @@ def spec_decode(shape, seed=3, max_new=256, ps=(0.6, 0.8, 0.95), statics=(1, 2, 
     return res
 
 
+def ep_shard_sweep(shape, G=2, ctx=1024, ks=(0, 2, 4, 8), seed=1):
+    """Expert-parallel shards measured one at a time on this one GPU
+    (CASCADE_EP_NOCOMM=1: no all-reduce).  The EP step on G GPUs costs the
+    max over ranks of these plus one all-reduce of T*(k+S)*d fp32 per layer,
+    which is reported as a byte count (not measured here)."""
+    os.environ["CASCADE_EP_NOCOMM"] = "1"
+    out = {}
+    try:
+        for r in range(G):
+            m = cb.Model(shape, seed, device=0, ep_rank=r, ep_size=G, nccl_id=bytes(128))
+            s = cb.Session(m, max_ctx=ctx + 64, k_max=15)
+            rng = np.random.default_rng(seed)
+            s.prefill(rng.integers(0, shape.vocab, ctx + 1).astype(np.int32))
+            st = torch.cuda.ExternalStream(s.stream(), device="cuda:0")
+            res = {}
+            for K in ks:
+                for _ in range(2):
+                    s.enqueue(K, commit=False)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(3):
+                    s.enqueue(K, commit=False)
+                e1.record(st)
+                s.sync()
+                U = float(np.mean(s.union_sizes()))
+                res[K] = {"latency_us": round(e0.elapsed_time(e1) / 3 * 1e3, 1), "unique_experts_per_layer": round(U, 3),
+                          "allreduce_bytes_per_layer": (K + 1) * (shape.top_k + shape.shared_experts) * shape.d_model * 4,
+                          "shard_bytes_gb": round(cb.model_bytes(shape, r, G) / 1e9, 1)}
+            out[f"rank{r}"] = res
+            s.close()
+            m.close()
+    finally:
+        os.environ.pop("CASCADE_EP_NOCOMM", None)
+    return out
+
+
 def scenario_sweep(shape, seed=5):
     """Reference scenario sweep (engine.hpp run_scenario) with verifier-backed cells:
     two tasks (a phased high/low-acceptance profile and a low-acceptance mix) x
@@ -146,6 +182,7 @@ def main():
                                                                        invariant=True)
     report["config4_qwen15_scenario"] = scenario_sweep(cb.preset("qwen15"))
     report["config2_mixtral_ctx4096"] = latency_sweep(cb.preset("mixtral"), ctx=4096, prompts=1)
+    report["config5_mixtral8x22b_ep2_shards"] = ep_shard_sweep(cb.preset("mixtral8x22b"), G=2)
     report["config5_mixtral8x22b_24layer_slice"] = latency_sweep(cb.preset("mixtral8x22b").with_layers(24), prompts=1)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     path = os.path.join(ROOT, "gpurun_out", f"configs_{TAG}.json")
