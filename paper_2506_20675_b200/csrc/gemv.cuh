@@ -371,7 +371,13 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     const bool routed = p.topk_id != nullptr;
     auto rk_row = [&](int bl) -> const signed char* { return routed ? un.rank[bl] : nullptr; };
     constexpr int kSlot = kTPW * NT * 32;
-    constexpr int kUnroll = NT == 1 ? 4 : 3;
+#ifndef CASCADE_KUNROLL1
+#define CASCADE_KUNROLL1 4
+#endif
+#ifndef CASCADE_KUNROLL2
+#define CASCADE_KUNROLL2 3
+#endif
+    constexpr int kUnroll = NT == 1 ? CASCADE_KUNROLL1 : CASCADE_KUNROLL2;  // k-steps of weights in flight per warp
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const uint64_t pol = policy_evict_first();
