@@ -626,10 +626,6 @@ struct cascade_session {
     float* attn_part = nullptr;
     uint16_t* attn_out = nullptr;
     float* logits_router = nullptr;
-    float* logit_part = nullptr;
-    float* ss_part = nullptr;
-    int* tok_ticket = nullptr;
-    int* ticket = nullptr;
     int* topk_id = nullptr;
     float* topk_w = nullptr;
     float* gsh = nullptr;
@@ -846,10 +842,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->attn_part, (size_t)D.KV * G * kMaxT * s->max_chunks * (D.hd + 2) * 4)) ||
         (rc = salloc(s, &s->attn_out, (size_t)D.hq * 32)) ||
         (rc = salloc(s, &s->logits_router, (size_t)kMaxT * (D.E + 1) * 4)) ||
-        (rc = salloc(s, &s->logit_part, (size_t)kMaxT * (D.d / kRouteSlice) * (D.E + 1) * 4)) ||
-        (rc = salloc(s, &s->ss_part, (size_t)kMaxT * (D.d / kRouteSlice) * 4)) ||
-        (rc = salloc(s, &s->tok_ticket, (size_t)kMaxT * 4)) ||
-        (rc = salloc(s, &s->ticket, 4)) || (rc = salloc(s, &s->topk_id, (size_t)kMaxT * D.k * 4)) ||
+        (rc = salloc(s, &s->topk_id, (size_t)kMaxT * D.k * 4)) ||
         (rc = salloc(s, &s->topk_w, (size_t)kMaxT * D.k * 4)) || (rc = salloc(s, &s->gsh, kMaxT * 4)) ||
         (rc = salloc(s, &s->list, (size_t)(nslots + 1) * 4)) || (rc = salloc(s, &s->count, 4)) ||
         (rc = salloc(s, &s->route_rank, (size_t)(nslots + 1) * kMaxT * 4)) ||
@@ -1316,8 +1309,6 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             c.xn_bfrag = next_umma ? s->xn_u : s->xn;
             c.umma = next_umma;
         }
-        c.ss_part = s->ss_part;
-        c.tok_ticket = s->tok_ticket;
         c.tap_moe = taps ? s->taps.moe_out + td : nullptr;
         c.tap_xn = (taps && l + 1 < D.L) ? s->taps.xn_attn + td + (size_t)kMaxT * D.d : nullptr;
         c.tap_x = (taps && l + 1 < D.L) ? s->taps.x_in + td + (size_t)kMaxT * D.d : nullptr;

@@ -1,20 +1,17 @@
-// moe.cuh — step entry (embedding), router + expert union, expert combine
-// (SURVEY.md §8(a2) stages K1/K2 and the epilogue of K3).
+// moe.cuh — step entry (embedding), router, expert combine
+// (SURVEY.md §8(a2) stage K1 and the epilogue of K3; the expert union, K2,
+// is built by every expert-GEMV CTA: gemv.cuh build_union).
 //
-// moe_route_kernel (grid = T tokens x router-row groups):
+// moe_route_kernel (grid = T, one CTA per token):
 //   1. RMSNorm of the residual row -> bf16 MoE input (B-frag layout for the
-//      expert GEMVs; written by the row-group-0 CTA of each token).
+//      expert GEMVs), 16-byte stores.
 //   2. Router logits: one warp per router row (E routed rows + the Qwen
-//      shared-expert gate row), bf16 weights, fp32 accumulate, all of a
-//      lane's 16-byte loads issued before any FMA.
-//   3. The last CTA to finish (atomic ticket) routes every token: softmax,
-//      top-k (larger logit first, lower expert index on ties), gate weights
-//      (renormalised over the k for Mixtral), then the expert union: OR of
-//      per-token 128-bit masks, ascending unique-expert list, per-expert
-//      token ranks.  This is the real counterpart of the reference's
-//      stand-ins draw_expert_set / sample_active_experts
-//      (expert_model.hpp:100-139): union = distinct routed experts, shared
-//      blocks always active on top.
+//      shared-expert gate row), bf16 weights staged in shared memory before
+//      the dependency wait when they fit, fp32 accumulate.
+//   3. Softmax and top-k (larger logit first, lower expert index on ties),
+//      gate weights (renormalised over the k for Mixtral): the real
+//      counterpart of the reference's stand-in draw_expert_set
+//      (expert_model.hpp:100-112).
 // moe_combine_kernel (grid = T): residual += sum_r w[t][r] * Y[t][r]
 //   (+ shared-gate * sum_b Y[t][k+b]) in fixed order, then the next RMSNorm
 //   (next layer's attention input, or the final norm).
@@ -29,20 +26,6 @@ constexpr int kRouteThreads = 256;
 constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kMaxExperts = 128;  // expert_model.hpp:96 (kMaxRoutedExperts)
 constexpr int kMaxTopK = 16;
-
-// 1/rms of one fp32 row (d % 4 == 0), block-wide.
-__device__ __forceinline__ float row_rinv(const float* x, int d, float eps, float* red) {
-    float ss = 0.f;
-    const float4* x4 = reinterpret_cast<const float4*>(x);
-    const int n4 = d >> 2;
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
-        const float4 v = x4[i];
-        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-    }
-    ss = block_sum(ss, red);
-    return 1.0f / sqrtf(ss / (float)d + eps);
-}
 
 struct RouteParams {
     const float* x;              // residual [T][d]
@@ -65,8 +48,6 @@ struct RouteParams {
     unsigned long long* trace;
 };
 
-constexpr int kRouteSlice = kRouteThreads;  // legacy slicing unit (d % 256 == 0)
-constexpr int kMaxSlices = 32;              // d <= 8192
 constexpr int kRowThreads = 512;            // route / combine: one CTA per token row
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
@@ -325,9 +306,7 @@ struct CombineParams {
     const float* gsh;            // [T]
     const uint16_t* norm_w;      // next norm weights [d]
     uint16_t* xn_bfrag;          // out
-    float* ss_part;              // scratch [T][n_slices] partial sums of squares
     int umma;                    // xn_bfrag in the UMMA B layout (dense tcgen05 GEMVs) instead of B-frag
-    int* tok_ticket;             // [T] arrival counters (zero between launches)
     float* tap_moe;              // optional [T][d] (the MoE contribution)
     uint16_t* tap_xn;            // optional [T][d] next-norm output
     float* tap_x;                // optional [T][d] residual after the add
