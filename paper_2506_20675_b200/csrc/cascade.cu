@@ -155,8 +155,20 @@ static int g_route_stage = 1;  // CASCADE_ROUTE_STAGE=0: read router rows from g
 static bool route_staged(const Dims& D, int shared_gate) {
     return g_route_stage && (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2 <= (size_t)kRouteStageBytes;
 }
+static int g_route_cluster = 1;  // CASCADE_ROUTE_CLUSTER=0: large routers read from global by one CTA
+// CTAs per token: routers larger than one CTA's staging budget are split
+// over a cluster so every row is staged in shared memory before the wait.
+static int route_cluster(const Dims& D, int shared_gate) {
+    const size_t bytes = (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2;
+    if (route_staged(D, shared_gate) || !g_route_cluster || !g_route_stage) return 1;
+    const int C = (int)((bytes + kRouteStageBytes - 1) / kRouteStageBytes);
+    return C <= 8 ? C : 1;
+}
 static size_t route_smem_bytes(const Dims& D, int shared_gate) {
-    return (size_t)D.d * 4 + (route_staged(D, shared_gate) ? (size_t)(D.E + (shared_gate ? 1 : 0)) * D.d * 2 : 0);
+    const int rows = D.E + (shared_gate ? 1 : 0);
+    const int C = route_cluster(D, shared_gate);
+    if (C > 1) return (size_t)D.d * 4 + (size_t)((rows + C - 1) / C) * D.d * 2;
+    return (size_t)D.d * 4 + (route_staged(D, shared_gate) ? (size_t)rows * D.d * 2 : 0);
 }
 
 static void local_experts(int E, int rank, int size, int& lo, int& hi) {
@@ -889,6 +901,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     else e = cudaFuncSetAttribute(attn_partial_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
     if (e == cudaSuccess) e = set_carveouts(D.hd);
     if (const char* v = getenv("CASCADE_ROUTE_STAGE")) g_route_stage = atoi(v);
+    if (const char* v = getenv("CASCADE_ROUTE_CLUSTER")) g_route_cluster = atoi(v);
     (void)0;
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(moe_route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -963,18 +976,23 @@ static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStrea
 
 
 
-// moe_route_kernel: T independent CTAs (one per token), PDL.
+// moe_route_kernel: one CTA (or a cluster of p.C CTAs) per token, PDL.
 static cudaError_t launch_route(const RouteParams& p, int T, size_t smem, cudaStream_t st) {
+    const int C = p.C > 1 ? p.C : 1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(T);
+    cfg.gridDim = dim3(T * C);
     cfg.blockDim = dim3(kRowThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = C;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = C > 1 ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, moe_route_kernel, p);
 }
 
@@ -1224,6 +1242,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.eps = m->g.norm_eps;
         rp.zero_nonlocal = m->ep_size > 1;
         rp.stage_w = route_staged(D, m->g.shared_gate);
+        rp.C = route_cluster(D, m->g.shared_gate);
         rp.stamp = s->stamps + 2 + 2 * l;
         rp.trace = tr(5);
         PB(5);

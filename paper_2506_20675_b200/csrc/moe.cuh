@@ -17,6 +17,8 @@
 //   (next layer's attention input, or the final norm).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "gemv_umma.cuh"
 
@@ -44,6 +46,7 @@ struct RouteParams {
     float eps;
     int zero_nonlocal;
     int stage_w;                 // router weights staged in smem before griddepcontrol.wait
+    int C;                       // > 1: cluster of C CTAs per token, each staging 1/C of the router rows
     unsigned long long* stamp;   // MoE-block start (CostBreakdown split)
     unsigned long long* trace;
 };
@@ -90,15 +93,25 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     const uint16_t* wsm = reinterpret_cast<const uint16_t*>(rsm + (size_t)p.d * 4);  // staged router rows
     __shared__ float red[32];
     __shared__ float s_lg[kMaxExperts + 1];
-    const int t = blockIdx.x;
+    // Large routers (OLMoE 64 x 2048, Qwen 61 x 2048) are split over a
+    // cluster of C CTAs per token: rank r stages rows [row_lo, row_hi) in
+    // its shared memory before the dependency wait, computes their logits
+    // into rank 0's shared memory (DSMEM), and rank 0 finishes the token
+    // after one cluster barrier (no global stores are pending at the
+    // barrier, so its release fence is cheap).
+    const int C = p.C > 1 ? p.C : 1;
+    const int t = blockIdx.x / C;
+    const int crank = blockIdx.x - t * C;
     const int n_rows = p.E + (p.shared_gate ? 1 : 0);
+    const int row_lo = n_rows * crank / C, row_hi = n_rows * (crank + 1) / C;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool staged = p.stage_w != 0;
+    const bool staged = p.stage_w != 0 || C > 1;
+    namespace cg = cooperative_groups;
     // ---- independent of the predecessor
     if (staged) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.router_w);
+        const uint4* src = reinterpret_cast<const uint4*>(p.router_w + (size_t)row_lo * p.d);
         uint4* dst = reinterpret_cast<uint4*>(rsm + (size_t)p.d * 4);
-        for (int i = threadIdx.x; i < n_rows * p.d / 8; i += kRowThreads) dst[i] = __ldg(src + i);
+        for (int i = threadIdx.x; i < (row_hi - row_lo) * p.d / 8; i += kRowThreads) dst[i] = __ldg(src + i);
     }
     constexpr int kPreIt = 8;  // 256 columns per chunk
     uint4 pre0[kPreIt];
@@ -120,7 +133,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     griddep_wait();
     griddep_launch_early();
     CTA_TRACE(p.trace);
-    if (t == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    if (t == 0 && crank == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
     phase_stamp(p.trace, 0);
     // ---- norm: thread owns groups of 8 consecutive columns (wide loads/stores)
     const float4* x4 = reinterpret_cast<const float4*>(p.x + (long long)t * p.d);
@@ -150,13 +163,15 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
         w[1] = pack_bf16((a.z * rinv) * bf16_lo(nw[j].y), (a.w * rinv) * bf16_hi(nw[j].y));
         w[2] = pack_bf16((b.x * rinv) * bf16_lo(nw[j].z), (b.y * rinv) * bf16_hi(nw[j].z));
         w[3] = pack_bf16((b.z * rinv) * bf16_lo(nw[j].w), (b.w * rinv) * bf16_hi(nw[j].w));
-        store_b8(p.xn_bfrag, false, t, 8 * c, w);
-        if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (C == 1) {
+            store_b8(p.xn_bfrag, false, t, 8 * c, w);
+            if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
         float4* xs4 = reinterpret_cast<float4*>(xs + 8 * c);
         xs4[0] = make_float4(bf16_lo(w[0]), bf16_hi(w[0]), bf16_lo(w[1]), bf16_hi(w[1]));
         xs4[1] = make_float4(bf16_lo(w[2]), bf16_hi(w[2]), bf16_lo(w[3]), bf16_hi(w[3]));
     }
-    if (p.zero_nonlocal) {
+    if (p.zero_nonlocal && C == 1) {
         // EP: every (token, rank) row is written by exactly one rank's down
         // GEMV; the others must contribute exact zeros to the all-reduce.
         float4* y = reinterpret_cast<float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
@@ -179,17 +194,18 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
         acc = fmaf(b.w, __uint_as_float(w.w & 0xFFFF0000u), acc);
         return acc;
     };
+    float* lg0 = C > 1 ? cg::this_cluster().map_shared_rank(s_lg, 0) : s_lg;  // rank 0's logits
     auto emit = [&](int e, float acc) {
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (lane == 0) {
-            s_lg[e] = acc;
-            p.logits[t * (p.E + 1) + e] = acc;
+            lg0[e] = acc;
+            if (C == 1) p.logits[t * (p.E + 1) + e] = acc;
         }
     };
     // n8 = d / 8 column groups (declared with the norm)
     if (staged) {
-        for (int e = warp; e < n_rows; e += kRowWarps) {
-            const uint4* w4 = reinterpret_cast<const uint4*>(wsm + (size_t)e * p.d);
+        for (int e = row_lo + warp; e < row_hi; e += kRowWarps) {
+            const uint4* w4 = reinterpret_cast<const uint4*>(wsm + (size_t)(e - row_lo) * p.d);
             float acc = 0.f;
 #pragma unroll 8
             for (int i = lane; i < n8; i += 32) acc = dot8(w4[i], i, acc);
@@ -235,6 +251,26 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
             }
             emit(e0, a0);
             if (has1) emit(e1, a1);
+        }
+    }
+    if (C > 1) {
+        cg::this_cluster().sync();  // every rank's logits are in rank 0's s_lg
+        if (crank != 0) return;
+        // rank 0: the deferred global writes (router logits, MoE input, EP zeros)
+        for (int e = threadIdx.x; e < n_rows; e += kRowThreads) p.logits[t * (p.E + 1) + e] = s_lg[e];
+#pragma unroll
+        for (int j = 0; j < kG; ++j) {
+            const int c = threadIdx.x + j * kRowThreads;
+            if (c >= n8) continue;
+            const float4* xs4 = reinterpret_cast<const float4*>(xs + 8 * c);
+            const float4 a = xs4[0], b = xs4[1];
+            uint32_t w[4] = {pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(b.x, b.y), pack_bf16(b.z, b.w)};
+            store_b8(p.xn_bfrag, false, t, 8 * c, w);
+            if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        if (p.zero_nonlocal) {
+            float4* y = reinterpret_cast<float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
+            for (int i = threadIdx.x; i < (p.k + p.S) * p.d / 4; i += kRowThreads) y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     __syncthreads();
