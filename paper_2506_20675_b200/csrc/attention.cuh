@@ -401,14 +401,18 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 // (row, 4 dims) per thread-item, the chunk loads of a batch of
                 // 9 chunks in flight together
                 constexpr int H4 = HD / 4;
+#ifndef CASCADE_ATTN_MB
+#define CASCADE_ATTN_MB 9
+#endif
+                constexpr int kMB = CASCADE_ATTN_MB;  // chunk partials in flight per (row, 4 dims)
                 for (int idx = threadIdx.x; idx < R * H4; idx += kAttnThreads) {
                     const int r = idx / H4, i = (idx - r * H4) * 4;
                     const float* pr = base + (long long)r * p.max_chunks * (HD + 2) + 2 + i;
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int c0 = 0; c0 < nck; c0 += 9) {
-                        float4 v9[9];
+                    for (int c0 = 0; c0 < nck; c0 += kMB) {
+                        float4 v9[kMB];
 #pragma unroll
-                        for (int u = 0; u < 9; ++u)
+                        for (int u = 0; u < kMB; ++u)
                             if (c0 + u < nck) {
                                 const float* q = pr + (long long)(c0 + u) * (HD + 2);  // 8-byte aligned: two float2
                                 const float2 lo = __ldcg(reinterpret_cast<const float2*>(q));
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                                 v9[u] = make_float4(lo.x, lo.y, hi.x, hi.y);
                             }
 #pragma unroll
-                        for (int u = 0; u < 9; ++u)
+                        for (int u = 0; u < kMB; ++u)
                             if (c0 + u < nck) {
                                 const float sc = scale[r * nck + c0 + u];
                                 acc.x = fmaf(v9[u].x, sc, acc.x);

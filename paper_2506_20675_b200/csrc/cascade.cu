@@ -1153,13 +1153,24 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         const int qrows = (G * T + 15) / 16 * 16;
         const int asm_ = D.hd == 32 ? attn_smem_bytes<32>(qrows) : D.hd == 64 ? attn_smem_bytes<64>(qrows)
                                                                                 : attn_smem_bytes<128>(qrows);
-        const int per_sm = std::max(1, std::min(4, (132 * 1024) / (asm_ + 2048)));
+        int per_sm = 1;  // resident CTAs per SM for this smem size (registers can bind first)
+        {
+            cudaError_t oe = D.hd == 32 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_partial_kernel<32>, kAttnThreads, asm_)
+                             : D.hd == 64 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_partial_kernel<64>, kAttnThreads, asm_)
+                                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, attn_partial_kernel<128>, kAttnThreads, asm_);
+            if (oe != cudaSuccess || per_sm < 1) {
+                cudaGetLastError();
+                per_sm = 1;
+            }
+            per_sm = std::min(per_sm, 4);
+        }
         const int agrid = m->num_sms * per_sm;
         // fused combine needs [R][chunks] + [R] floats of the kernel's smem
         // and is only worth it while one CTA can keep every load in flight
         // (one (row, 4-dim) item per thread); wider T use attn_combine
+        // (and short contexts: the merge loads 9 chunk partials per round trip)
         const bool fused = s->attn_fused && ((long long)(G * T) * (2 * s->max_chunks + 1)) * 4 <= asm_ &&
-                           G * T * (D.hd / 4) <= kAttnThreads;
+                           G * T * (D.hd / 4) <= kAttnThreads && s->max_chunks <= 27;
         ap.fused = fused;
         ap.arrive = s->attn_arrive;
         ap.out_bfrag = s->attn_out;
