@@ -379,36 +379,66 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     const int n4 = p.d >> 2;
     const int nr = p.k + p.S;
     const float g = p.gsh[t];
+    float wk[8];  // the token's gate weights (rows 0..k-1 of its contribution list)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) wk[q] = q < p.k ? p.topk_w[t * p.k + q] : 0.f;
     float4 nx[kG][2];
     float ss = 0.f;
 #pragma unroll
     for (int j = 0; j < kG; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= n8) continue;
+        // every load of the group issued before any math: both halves of the
+        // residual and of up to kMaxR contribution rows (sums in row order)
+        constexpr int kMaxR = 8;
+        float4 x0v[2], yb[kMaxR][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) x0v[h] = x4[2 * c + h];
+#pragma unroll
+        for (int q = 0; q < kMaxR; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (q < nr) yb[q][h] = y4[(long long)q * n4 + 2 * c + h];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = 2 * c + h;
-            const float4 x0 = x4[i];
+            const float4 x0 = x0v[h];
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int r0 = 0; r0 < nr; r0 += 4) {  // loads in batches of 4 rows, sums in row order
-                float4 yb[4];
+#pragma unroll
+            for (int q = 0; q < kMaxR; ++q) {
+                if (q >= nr) break;
+                if (q < p.k) {
+                    const float w = wk[q];
+                    acc.x += w * yb[q][h].x;
+                    acc.y += w * yb[q][h].y;
+                    acc.z += w * yb[q][h].z;
+                    acc.w += w * yb[q][h].w;
+                } else {
+                    sh.x += yb[q][h].x;
+                    sh.y += yb[q][h].y;
+                    sh.z += yb[q][h].z;
+                    sh.w += yb[q][h].w;
+                }
+            }
+            for (int r0 = kMaxR; r0 < nr; r0 += 4) {  // rows beyond kMaxR: batches of 4, row order
+                float4 yr[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (r0 + q < nr) yb[q] = y4[(long long)(r0 + q) * n4 + i];
+                    if (r0 + q < nr) yr[q] = y4[(long long)(r0 + q) * n4 + i];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q;
                     if (r < p.k) {
                         const float w = p.topk_w[t * p.k + r];
-                        acc.x += w * yb[q].x;
-                        acc.y += w * yb[q].y;
-                        acc.z += w * yb[q].z;
-                        acc.w += w * yb[q].w;
+                        acc.x += w * yr[q].x;
+                        acc.y += w * yr[q].y;
+                        acc.z += w * yr[q].z;
+                        acc.w += w * yr[q].w;
                     } else if (r < nr) {
-                        sh.x += yb[q].x;
-                        sh.y += yb[q].y;
-                        sh.z += yb[q].z;
-                        sh.w += yb[q].w;
+                        sh.x += yr[q].x;
+                        sh.y += yr[q].y;
+                        sh.z += yr[q].z;
+                        sh.w += yr[q].w;
                     }
                 }
             }
