@@ -883,7 +883,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_O")) s->pf_o = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = v[0] == '1';
-    if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = v[0] == '1';
+    if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = atoi(v);  // 1: whole range, n > 1: first n k-steps
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';

@@ -59,7 +59,7 @@ struct GemvParams {
     unsigned long long* stamp; // optional globaltimer stamp at kernel start
     unsigned long long* trace; // in-graph trace slot
     int early_list;            // list/count final before griddepcontrol.wait (expert down projection)
-    int l2_prologue;           // also L2-prefetch the rest of each warp's range before the wait
+    int l2_prologue;           // also L2-prefetch each warp's range before the wait: 0 off, 1 all, n > 1: the first n k-steps
     int trigger;               // griddepcontrol.launch_dependents right after the wait
     // Routed blocks: when topk_id is set, every CTA builds the expert union
     // itself from the router's top-k (no separate union kernel, no
@@ -437,11 +437,12 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
             }
             if (p.l2_prologue && lane == 0) {
                 // the rest of this warp's range -> L2 while the predecessor drains
-                for (long long pos = pf_from; pos < whi0;) {
+                const long long pf_to = p.l2_prologue > 1 && wlo0 + p.l2_prologue < whi0 ? wlo0 + p.l2_prologue : whi0;
+                for (long long pos = pf_from; pos < pf_to;) {
                     const long long unit = pos / p.n_ks;
                     const int ks = (int)(pos - unit * p.n_ks);
                     long long n = p.n_ks - ks;
-                    if (whi0 - pos < n) n = whi0 - pos;
+                    if (pf_to - pos < n) n = pf_to - pos;
                     const int bl = (int)(unit / p.n_st);
                     const int st = (int)(unit - (long long)bl * p.n_st);
                     const int blk = routed ? un.list[bl] : (p.list ? __ldcg(p.list + bl) : bl);
