@@ -662,6 +662,10 @@ struct cascade_session {
     int down_early = 1;
     int umma_prologue = 1;
     int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
+    int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
+    float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
+    int* counters2 = nullptr;
+    int* ffn_ready = nullptr;    // [slots] published gate/up super-tiles
     int invariant = 0;     // batch-invariant expert GEMV split (bitwise-lossless speculation)
     int* sm_index = nullptr;   // %smid -> dense SM index (SM-weighted expert GEMV split), nullptr: off
     int* sm_slot = nullptr;
@@ -862,6 +866,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->hbuf, (size_t)std::max(nslots, 1) * D.f * 32)) ||
         (rc = salloc(s, &s->ycontrib, (size_t)kMaxT * (D.k + D.S) * D.d * 4)) ||
         (rc = salloc(s, &s->partial, (size_t)std::max<long long>(workers, (long long)nslots * s->gemv_grid) * 2 * kTPW * 2 * 32 * 16, false)) ||
+        (rc = salloc(s, &s->partial2, (size_t)std::max<long long>(workers, (long long)nslots * s->gemv_grid) * 2 * kTPW * 2 * 32 * 16, false)) ||
+        (rc = salloc(s, &s->counters2, (size_t)max_units * 4)) || (rc = salloc(s, &s->ffn_ready, (size_t)(nslots + 1) * 4)) ||
         (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->attn_arrive, (size_t)D.KV * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
         (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
@@ -888,6 +894,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
     if (const char* v = getenv("CASCADE_ATTN_FUSED")) s->attn_fused = v[0] == '1';
+    if (const char* v = getenv("CASCADE_FFN_FUSED")) s->ffn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
@@ -911,6 +918,10 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = cudaFuncSetAttribute(stream_gemv_umma_kernel<UEPI_ARGMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_umma_smem_bytes());
     if (e == cudaSuccess) e = gemv_smem_attr<1>();
     if (e == cudaSuccess) e = gemv_smem_attr<2>();
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_smem_bytes<1>());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_smem_bytes<2>());
+    if (e == cudaSuccess) e = carve(expert_ffn_kernel<1>);
+    if (e == cudaSuccess) e = carve(expert_ffn_kernel<2>);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
@@ -969,6 +980,10 @@ static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaSt
     case EPI_DOWN: return launch_k(stream_gemv_kernel<NT, EPI_DOWN>, grid, kGemvThreads, sm, st, pdl, p);
     default: return launch_k(stream_gemv_kernel<NT, EPI_ARGMAX>, grid, kGemvThreads, sm, st, pdl, p);
     }
+}
+static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st) {
+    if (f.gu.T <= 8) return launch_k(expert_ffn_kernel<1>, grid, kGemvThreads, gemv_smem_bytes<1>(), st, true, f);
+    return launch_k(expert_ffn_kernel<2>, grid, kGemvThreads, gemv_smem_bytes<2>(), st, true, f);
 }
 static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStream_t st, bool pdl = true) {
     return p.T <= 8 ? launch_gemv_nt<1>(epi, p, grid, st, pdl) : launch_gemv_nt<2>(epi, p, grid, st, pdl);
@@ -1300,10 +1315,6 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         gu.hout = s->hbuf;
         gu.h_block_stride = (long long)D.f * 16;
         gu.trace = tr(6);
-        PB(6);
-        CK(launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st));
-        PE();
-        ++nk;
         GemvParams dn = gemv_base(s, T);
         dn.W = w.w2;
         dn.w_block_stride = D.w2_vec;
@@ -1316,11 +1327,29 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         dn.n_contrib = D.k + D.S;
         dn.out = s->ycontrib;
         dn.ld = D.d;
-        dn.trace = tr(7);
-        PB(7);
-        CK(launch_gemv(EPI_DOWN, dn, s->gemv_grid, st));
-        PE();
-        ++nk;
+        if (s->ffn_fused) {
+            FfnParams fp{};
+            fp.gu = gu;
+            fp.dn = dn;
+            fp.dn.partial = s->partial2;
+            fp.dn.counters = s->counters2;
+            fp.ready = s->ffn_ready;
+            fp.n_st_gu = gu.n_st;
+            PB(6);
+            CK(launch_ffn(fp, s->gemv_grid, st));
+            PE();
+            ++nk;
+        } else {
+            PB(6);
+            CK(launch_gemv(EPI_GATEUP, gu, s->gemv_grid, st));
+            PE();
+            ++nk;
+            dn.trace = tr(7);
+            PB(7);
+            CK(launch_gemv(EPI_DOWN, dn, s->gemv_grid, st));
+            PE();
+            ++nk;
+        }
         if (m->comm) {
             PB(11);
             const int nr = g_nccl.AllReduce(s->ycontrib, s->ycontrib, (size_t)T * (D.k + D.S) * D.d, kNcclFloat32,
@@ -1329,6 +1358,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             if (nr != 0) return set_err(CASCADE_ERUNTIME, "ncclAllReduce failed");
         }
         CombineParams c{};
+        c.ffn_ready = s->ffn_fused ? s->ffn_ready : nullptr;
+        c.n_ready = m->n_blocks;
         c.x = s->x;
         c.ycontrib = s->ycontrib;
         c.topk_w = s->topk_w;

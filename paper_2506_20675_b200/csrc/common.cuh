@@ -148,6 +148,13 @@ __device__ __forceinline__ uint2 ldg_act(const uint2* p) {
     return v;
 }
 
+// Activations written earlier in the same launch (fused expert FFN): L2 only.
+__device__ __forceinline__ uint2 ldcg_act(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint4& a, const uint2& b) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 "

@@ -607,4 +607,216 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     }
 }
 
+// One phase of the fused expert FFN (expert_ffn_kernel): the stream-K work
+// of stream_gemv_kernel for one matrix.  Phase 0 (gate/up) counts each
+// finished super-tile of slot bl in s_done[bl]; phase 1 (down) waits, per
+// slot, until ready[bl] reaches target (every gate/up super-tile of that
+// expert published) and reads its B operand (SiLU(gate)*up, written in this
+// launch) from L2.
+template <int NT, int EPI, bool WAIT>
+__device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& un, int wi, int* s_done,
+                                          const int* ready, int target) {
+    extern __shared__ float4 red[];
+    __shared__ long long seg_unit[kGemvWarps][2];
+    const bool routed = true;
+    auto rk_row = [&](int bl) -> const signed char* { return un.rank[bl]; };
+    constexpr int kSlot = kTPW * NT * 32;
+    constexpr int kUnroll = NT == 1 ? CASCADE_KUNROLL1 : CASCADE_KUNROLL2;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint64_t pol = policy_evict_first();
+    uint4 a[kUnroll][kTPW];
+    bool pre = false;
+    unsigned long long ready_mask[WAIT ? (kMaxSlots + 63) / 64 : 1] = {};
+    (void)kSlot;
+    const int U = routed ? un.count : (p.count ? *p.count : p.n_blocks);
+    const long long per_block = (long long)p.n_st * p.n_ks * (p.invariant ? 1 : U);
+    const int n_blocks_w = p.invariant ? U : (U > 0 ? 1 : 0);
+    const int P = block_pieces(p, per_block);
+    const int n_items = n_blocks_w * P;
+    float acc[kTPW][NT][4];
+    constexpr int kMaxPend = 2 * kMaxSlots;  // <= 2 boundary super-tiles per item
+    __shared__ int4 pend[kMaxPend];
+    __shared__ int n_pend;
+    if (threadIdx.x == 0) n_pend = 0;
+    __syncthreads();
+    for (int item = wi; item < n_items; item += gridDim.x) {
+        const int b = item / P, q = item - b * P;
+        // this piece of block b, in flat (unit, k-step) positions
+        const long long base = (long long)b * per_block;
+        const long long clo = base + piece_start(per_block, q, P, p.cum), chi = base + piece_start(per_block, q + 1, P, p.cum);
+        const long long wlo = clo + (chi - clo) * warp / kGemvWarps;
+        const long long whi = clo + (chi - clo) * (warp + 1) / kGemvWarps;
+        if (lane == 0) {
+            seg_unit[warp][0] = -1;
+            seg_unit[warp][1] = -1;
+        }
+        __syncwarp();
+
+        long long pos = wlo;
+        while (pos < whi) {
+            const long long unit = pos / p.n_ks;
+            const int ks0 = (int)(pos - unit * p.n_ks);
+            const long long rem = whi - pos;
+            const int ks1 = rem < (long long)(p.n_ks - ks0) ? ks0 + (int)rem : p.n_ks;
+            const int bl = (int)(unit / p.n_st);
+            const int st = (int)(unit - (long long)bl * p.n_st);
+            const int blk = routed ? un.list[bl] : (p.list ? p.list[bl] : bl);
+            if constexpr (WAIT) {
+                if (!((ready_mask[bl >> 6] >> (bl & 63)) & 1ull)) {
+                    if (lane == 0) {
+                        long long spins = 0;
+                        int v;
+                        for (;;) {
+                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready + bl) : "memory");
+                            if (v >= target) break;
+                            if (++spins > (1ll << 22)) __trap();  // a lost producer must not hang the GPU (~seconds)
+                            __nanosleep(64);
+                        }
+                    }
+                    __syncwarp();
+                    ready_mask[bl >> 6] |= 1ull << (bl & 63);
+                }
+            }
+            const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
+            const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
+            zero_acc<NT>(acc);
+            int s = ks0;
+            for (; s + kUnroll <= ks1; s += kUnroll) {
+                uint2 bb[kUnroll][NT];
+                if (!pre) {
+#pragma unroll
+                    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                        for (int it = 0; it < kTPW; ++it)
+                            a[u][it] = ldg_stream(A + ((long long)(s + u) * kTPW + it) * 32, pol);
+                }
+                pre = false;
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) bb[u][nt] = WAIT ? ldcg_act(Bp + ((s + u) * 2 + nt) * 32) : ldg_act(Bp + ((s + u) * 2 + nt) * 32);
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                    for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], bb[u][nt]);
+            }
+            for (; s < ks1; ++s) {
+                uint4 a1[kTPW];
+                uint2 bb[NT];
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it) a1[it] = ldg_stream(A + ((long long)s * kTPW + it) * 32, pol);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) bb[nt] = WAIT ? ldcg_act(Bp + (s * 2 + nt) * 32) : ldg_act(Bp + (s * 2 + nt) * 32);
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], bb[nt]);
+            }
+            const bool first_seg = pos == wlo;
+            pos += ks1 - ks0;
+            if (ks0 == 0 && ks1 == p.n_ks) {
+                gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
+                if constexpr (!WAIT) { if (lane == 0) atomicAdd(s_done + bl, 1); }
+            } else {
+                const int slot = first_seg ? 0 : 1;
+                store_acc<NT>(red + (warp * 2 + slot) * kSlot + lane, acc, false);
+                if (lane == 0) seg_unit[warp][slot] = unit;
+            }
+        }
+        __syncthreads();
+
+        // ---- piece-level reduction of split super-tiles (owner = first contributor)
+        for (int slot = 0; slot < 2; ++slot) {
+            const long long unit = seg_unit[warp][slot];
+            if (unit < 0) continue;
+            bool owner = true;
+            for (int w = 0; w < warp && owner; ++w) owner = seg_unit[w][0] != unit && seg_unit[w][1] != unit;
+            if (!owner) continue;
+            zero_acc<NT>(acc);
+            add_acc<NT>(acc, red + (warp * 2 + slot) * kSlot + lane, false);
+            for (int w = warp + 1; w < kGemvWarps; ++w)
+                for (int s2 = 0; s2 < 2; ++s2)
+                    if (seg_unit[w][s2] == unit) add_acc<NT>(acc, red + (w * 2 + s2) * kSlot + lane, false);
+            const long long ustart = unit * p.n_ks, uend = ustart + p.n_ks;
+            const int bl = (int)(unit / p.n_st);
+            const int st = (int)(unit - (long long)bl * p.n_st);
+            if (ustart >= clo && uend <= chi) {
+                gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
+                if constexpr (!WAIT) { if (lane == 0) atomicAdd(s_done + bl, 1); }
+                continue;
+            }
+            // crosses a piece boundary: store the piece partial now, count the
+            // arrival after the CTA's last item (one fence for all of them)
+            const int first = piece_owner(ustart - base, per_block, P, p.cum);
+            const int last = piece_owner(uend - 1 - base, per_block, P, p.cum);
+            const int gslot = (q == first) ? 1 : 0;
+            store_acc<NT>(p.partial + (((long long)b * P + q) * 2 + gslot) * kSlot + lane, acc, true);
+            if (lane == 0) {
+                const int i = atomicAdd(&n_pend, 1);
+                if (i < kMaxPend) pend[i] = make_int4((int)unit, b, first, last);
+            }
+        }
+        __syncthreads();  // red[] / seg_unit reused by the next item
+    }
+    // ---- cross-piece reductions: every piece partial of this CTA is stored;
+    //      one fence, then the arrivals; the last arriving piece of a
+    //      super-tile sums the piece partials in piece order
+    __threadfence();
+    __syncthreads();
+    const int np = n_pend < kMaxPend ? n_pend : kMaxPend;
+    for (int e = warp; e < np; e += kGemvWarps) {
+        const int4 pe = pend[e];
+        const long long unit = pe.x;
+        const int b = pe.y, first = pe.z, last = pe.w;
+        int prev = 0;
+        if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev != last - first) continue;
+        __threadfence();
+        zero_acc<NT>(acc);
+        for (int j = first; j <= last; ++j)
+            add_acc<NT>(acc, p.partial + (((long long)b * P + j) * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
+        if (lane == 0) p.counters[unit] = 0;
+        const int bl = (int)(unit / p.n_st);
+        const int st = (int)(unit - (long long)bl * p.n_st);
+        gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
+                if constexpr (!WAIT) { if (lane == 0) atomicAdd(s_done + bl, 1); }
+    }
+}
+
+struct FfnParams {
+    GemvParams gu, dn;         // expert gate/up (EPI_GATEUP) and down (EPI_DOWN) launches' parameters
+    int* ready;                // [slots] published gate/up super-tiles (zeroed by the combine kernel)
+    int n_st_gu;               // gate/up super-tiles per expert
+};
+
+// Fused expert FFN: gate/up (+SiLU) and down in one launch of 2 CTAs per SM
+// (all co-resident), so the down projection needs no second launch, no
+// kernel-boundary gap and no late-starting CTAs.  A CTA finishes its
+// gate/up range, publishes the super-tiles it completed per expert (one
+// fence), and streams its down range; a down segment of expert b starts
+// once every gate/up super-tile of b is published.
+template <int NT>
+__global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f) {
+    __shared__ UnionSmem un;
+    __shared__ int s_done[kMaxSlots];
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) s_done[i] = 0;
+    griddep_wait();
+    if (f.gu.trigger) griddep_launch();
+    CTA_TRACE(f.gu.trace);
+    if (warp == 0) build_union(f.gu, un);
+    __syncthreads();
+    if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
+    ffn_phase<NT, EPI_GATEUP, false>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
+    __threadfence();
+    __syncthreads();
+    for (int i = threadIdx.x; i < un.count; i += blockDim.x)
+        if (s_done[i] > 0) atomicAdd(f.ready + i, s_done[i]);
+    ffn_phase<NT, EPI_DOWN, true>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
+}
+
 }  // namespace cascade

@@ -351,6 +351,8 @@ struct CombineParams {
     const void* pf;              // next layer's QKV weights -> L2
     unsigned long long pf_bytes;
     unsigned long long* trace;
+    int* ffn_ready;              // fused expert FFN readiness counters, zeroed here for the next layer
+    int n_ready;
 };
 
 // grid = T CTAs of 512 threads, one token row each; thread owns groups of
@@ -374,6 +376,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     phase_stamp(p.trace, 0);
+    if (p.ffn_ready != nullptr && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < p.n_ready; i += blockDim.x) p.ffn_ready[i] = 0;
     const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
     float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
     const int n4 = p.d >> 2;
