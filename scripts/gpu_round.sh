@@ -21,7 +21,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-
   --log-file gpurun_out/launches_$TAG.csv python scripts/profile_step.py --ks 0,8 > gpurun_out/prof_launch_$TAG.log 2>&1
 echo "ncu1 rc=$?" >> gpurun_out/prof_launch_$TAG.log
 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:"stream_gemv|dense_gemv_cluster" -c 10 -o gpurun_out/gemv_full_$TAG python scripts/profile_step.py --ks 8 --layers 2 > gpurun_out/prof_full_$TAG.log 2>&1
+  -k regex:"stream_gemv|dense_gemv_cluster|expert_ffn" -c 10 -o gpurun_out/gemv_full_$TAG python scripts/profile_step.py --ks 8 --layers 2 > gpurun_out/prof_full_$TAG.log 2>&1
 echo "ncu2 rc=$?" >> gpurun_out/prof_full_$TAG.log
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
   -k regex:"moe_route|moe_combine|attn_partial|attn_combine" -c 8 -o gpurun_out/small_full_$TAG python scripts/profile_step.py --ks 0 --layers 2 > gpurun_out/prof_small_$TAG.log 2>&1

@@ -19,6 +19,9 @@ def cls(n):
     m = re.search(r"dense_gemv_cluster_kernel<\(?[a-z]*\)?(\d)", n)
     if m:
         return f"tcgen05 cluster split-K {EPI[m.group(1)]}"
+    m = re.search(r"expert_ffn_kernel<\(?[a-z]*\)?(\d)>", n)
+    if m:
+        return f"mma.sync fused expert FFN NT={m.group(1)} (gate/up + down)"
     m = re.search(r"stream_gemv_kernel<\(?[a-z]*\)?(\d), \(?[a-z]*\)?(\d)>", n)
     if m:
         return f"mma.sync gemv NT={m.group(1)} {EPI[m.group(2)]}"
