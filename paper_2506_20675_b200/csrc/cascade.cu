@@ -1269,6 +1269,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.zero_nonlocal = m->ep_size > 1;
         rp.stage_w = route_staged(D, m->g.shared_gate);
         rp.C = route_cluster(D, m->g.shared_gate);
+        rp.ffn_ready = s->ffn_fused ? s->ffn_ready : nullptr;
+        rp.n_ready = m->n_blocks;
         rp.stamp = s->stamps + 2 + 2 * l;
         rp.trace = tr(5);
         PB(5);
@@ -1358,8 +1360,6 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             if (nr != 0) return set_err(CASCADE_ERUNTIME, "ncclAllReduce failed");
         }
         CombineParams c{};
-        c.ffn_ready = s->ffn_fused ? s->ffn_ready : nullptr;
-        c.n_ready = m->n_blocks;
         c.x = s->x;
         c.ycontrib = s->ycontrib;
         c.topk_w = s->topk_w;

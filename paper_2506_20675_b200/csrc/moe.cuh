@@ -47,6 +47,8 @@ struct RouteParams {
     int zero_nonlocal;
     int stage_w;                 // router weights staged in smem before griddepcontrol.wait
     int C;                       // > 1: cluster of C CTAs per token, each staging 1/C of the router rows
+    int* ffn_ready;              // fused expert FFN readiness counters: zeroed here, before this layer's FFN
+    int n_ready;
     unsigned long long* stamp;   // MoE-block start (CostBreakdown split)
     unsigned long long* trace;
 };
@@ -134,6 +136,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     griddep_launch_early();
     CTA_TRACE(p.trace);
     if (t == 0 && crank == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
+    if (p.ffn_ready != nullptr && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < p.n_ready; i += blockDim.x) p.ffn_ready[i] = 0;
     phase_stamp(p.trace, 0);
     // ---- norm: thread owns groups of 8 consecutive columns (wide loads/stores)
     const float4* x4 = reinterpret_cast<const float4*>(p.x + (long long)t * p.d);
@@ -351,8 +355,6 @@ struct CombineParams {
     const void* pf;              // next layer's QKV weights -> L2
     unsigned long long pf_bytes;
     unsigned long long* trace;
-    int* ffn_ready;              // fused expert FFN readiness counters, zeroed here for the next layer
-    int n_ready;
 };
 
 // grid = T CTAs of 512 threads, one token row each; thread owns groups of
@@ -376,8 +378,6 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     phase_stamp(p.trace, 0);
-    if (p.ffn_ready != nullptr && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < p.n_ready; i += blockDim.x) p.ffn_ready[i] = 0;
     const float4* y4 = reinterpret_cast<const float4*>(p.ycontrib + (long long)t * (p.k + p.S) * p.d);
     float4* x4 = reinterpret_cast<float4*>(p.x + (long long)t * p.d);
     const int n4 = p.d >> 2;
