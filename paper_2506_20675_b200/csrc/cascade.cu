@@ -662,6 +662,7 @@ struct cascade_session {
     int down_early = 1;
     int umma_prologue = 1;
     int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
+    int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
     int* counters2 = nullptr;
@@ -674,6 +675,7 @@ struct cascade_session {
     int* attn_arrive = nullptr;
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
     int pf_o = 0;          // attention CTAs (the whole grid) bulk-prefetch W_o into L2 after their wait
+    int umma_no_trigger = 0;  // A/B: tcgen05 GEMVs let their dependents launch only at exit
     int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
     int o_cluster = 0;     // same for the O projection
@@ -889,12 +891,14 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_O")) s->pf_o = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = v[0] == '1';
+    if (const char* v = getenv("CASCADE_UMMA_TRIGGER")) s->umma_no_trigger = v[0] == '0';
     if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = atoi(v);  // 1: whole range, n > 1: first n k-steps
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_DOWN_EARLY")) s->down_early = v[0] == '1';
     if (const char* v = getenv("CASCADE_UMMA_PROLOGUE")) s->umma_prologue = v[0] == '1';
     if (const char* v = getenv("CASCADE_ATTN_FUSED")) s->attn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FUSED")) s->ffn_fused = v[0] == '1';
+    if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
@@ -1029,6 +1033,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.no_prologue = !s->umma_prologue;
     p.ring_stages = s->cluster_stages;
     p.pf_self = s->pf_self;
+    p.no_trigger = s->umma_no_trigger;
     return p;
 }
 
@@ -1337,6 +1342,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             fp.dn.counters = s->counters2;
             fp.ready = s->ffn_ready;
             fp.n_st_gu = gu.n_st;
+            // dependents launch at exit: an early-resident combine CTA made
+            // its own loads 2x slower (A/B, profiles/r01f/ab_ffn_trigger.txt)
+            fp.gu.trigger = s->ffn_trigger;
             PB(6);
             CK(launch_ffn(fp, s->gemv_grid, st));
             PE();

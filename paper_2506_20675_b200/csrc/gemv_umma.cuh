@@ -118,6 +118,7 @@ struct UGemvParams {
     int no_prologue;           // A/B: issue nothing before griddepcontrol.wait
     int ring_stages;           // dense_gemv_cluster_kernel: ring depth (<= kCMaxStages)
     int pf_self;               // dense_gemv_cluster_kernel: L2-prefetch the k-range beyond the ring before the wait
+    int no_trigger;            // 1: dependents launch at exit, not right after the wait
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
             };
             if (early && lane == 0 && !p.no_prologue) issue(kUStages, false);  // PDL prologue: weights overlap the predecessor's tail
             griddep_wait();
-            griddep_launch();
+            if (!p.no_trigger) griddep_launch();
             if (lane != 0) goto producer_done;
             udbg(p, 1);
             for (int j = 0; j < (PROBE == 2 ? 0 : n_pre); ++j)
@@ -390,7 +391,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
     } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issuer
         griddep_wait();
-        griddep_launch();
+        if (!p.no_trigger) griddep_launch();
         if (lane == 0) {
             const int U = p.count ? *p.count : p.n_blocks;
             const UWork w = uwork(p, U);
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
     } else {
         // ------------------------------------------------------------ epilogue (warps 0-3)
         griddep_wait();
-        griddep_launch();
+        if (!p.no_trigger) griddep_launch();
         trace_start(p.trace);
         if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
         if (threadIdx.x == 0) udbg(p, 5);
@@ -628,7 +629,7 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
             }
         }
         griddep_wait();
-        griddep_launch();
+        if (!p.no_trigger) griddep_launch();
         if (lane == 0) {
             for (int i = 0; i < n_stages; ++i) {
                 const int slot = i % NS;
@@ -646,7 +647,7 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
     } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issuer
         griddep_wait();
-        griddep_launch();
+        if (!p.no_trigger) griddep_launch();
         if (lane == 0) {
             const int n_stages = (ks_hi - ks_lo + kUStageKs - 1) / kUStageKs;
             bool first = true;
@@ -670,7 +671,7 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
     } else {
         // ------------------------------------------------------------ epilogue (warps 0-3, thread = row)
         griddep_wait();
-        griddep_launch();
+        if (!p.no_trigger) griddep_launch();
         trace_start(p.trace);
         if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
         const int r = warp * 32 + lane;
