@@ -661,7 +661,7 @@ struct cascade_session {
     int gemv_trigger = 1;  // early launch_dependents: the down GEMV builds its union and requests its first weights while gate/up drains
     int down_early = 1;
     int umma_prologue = 1;
-    int attn_fused = 1;    // chunk combine inside the attention kernel (last item per KV head)
+    int attn_fused = 0;    // chunk combine inside the attention kernel (last item per KV head); A/B: the separate combine is as fast or faster
     int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
