@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         kv_pending = true;
     }
     griddep_wait();
-    griddep_launch_early();
+    griddep_launch_early(kLateAttn);
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     const int n_items = nch * p.KV;
@@ -463,7 +463,7 @@ constexpr int kMaxChunksSmem = 1024;
 
 __global__ void attn_combine_kernel(AttnCombineParams p) {
     griddep_wait();
-    griddep_launch_early();
+    griddep_launch_early(kLateAttnCombine);
     CTA_TRACE(p.trace);
     __shared__ float scale_c[kMaxChunksSmem];
     __shared__ float red[32];

@@ -902,7 +902,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
-        const int late = v[0] == '1';
+        const int late = (v[0] == '1' && v[1] == 0) ? 31 : atoi(v);  // "1": every latency-bound kernel; else a kLate* mask
         cudaMemcpyToSymbol(g_late_trigger, &late, sizeof(late));
     }
     // attention smem opt-in

@@ -41,12 +41,13 @@ __device__ __forceinline__ uint64_t globaltimer_raw() {
 // rasterisation overlap the predecessor's tail.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-// A/B switch (CASCADE_LATE_TRIGGER=1): latency-bound kernels let their
-// dependents launch only at exit, so the next GEMV's weight prologue does
-// not compete with their loads.
+// A/B switch (CASCADE_LATE_TRIGGER=1 for all, or a mask of kLate*):
+// latency-bound kernels let their dependents launch only at exit, so the
+// next GEMV's weight prologue does not compete with their loads.
+enum { kLateAttn = 1, kLateAttnCombine = 2, kLateRoute = 4, kLateCombine = 8, kLateEmbed = 16 };
 __device__ int g_late_trigger = 0;
-__device__ __forceinline__ void griddep_launch_early() {
-    if (!g_late_trigger) griddep_launch();
+__device__ __forceinline__ void griddep_launch_early(int kind) {
+    if (!(g_late_trigger & kind)) griddep_launch();
 }
 
 // Bulk L2 prefetch of an upcoming weight matrix, spread over every thread

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
         nw[j] = c < (p.d >> 3) ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
     }
     griddep_wait();
-    griddep_launch_early();
+    griddep_launch_early(kLateRoute);
     CTA_TRACE(p.trace);
     if (t == 0 && crank == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
     if (p.ffn_ready != nullptr && blockIdx.x == 0)
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
         nw[j] = c < n8 ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
     }
     griddep_wait();
-    griddep_launch_early();
+    griddep_launch_early(kLateCombine);
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     phase_stamp(p.trace, 0);
@@ -522,7 +522,7 @@ struct EmbedParams {
 
 __global__ void __launch_bounds__(kRouteThreads) embed_norm_kernel(EmbedParams p) {
     griddep_wait();
-    griddep_launch_early();
+    griddep_launch_early(kLateEmbed);
     CTA_TRACE(p.trace);
     prefetch_l2(p.pf, p.pf_bytes);
     __shared__ float red[32];
