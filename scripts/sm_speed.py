@@ -1,3 +1,5 @@
+"""Diagnostic: per-SM streaming rate of the expert GEMV CTAs (from the per-CTA
+timeline), used to test the SM-rate-weighted split (rejected)."""
 import sys, os, numpy as np
 sys.path.insert(0, '/root/repo')
 import paper_2506_20675_b200 as cb
