@@ -266,6 +266,26 @@ def test_rejects_bad_requests(tiny):
     s.close()
 
 
+def test_kv_cache_bounds(tiny):
+    """The session's KV capacity is enforced: a prefill that would not leave
+    room for a full-width step is rejected (EINVAL), and the verify that
+    fills the cache reports it (ERUNTIME, after committing: the session
+    keeps kMaxT rows of headroom past max_ctx for the in-flight tokens)
+    instead of letting the next step write past the end."""
+    shape, m, om = tiny
+    s = cb.Session(m, max_ctx=48, k_max=4)
+    with pytest.raises(ValueError):
+        s.prefill(prompt(60, seed=2))
+    s.prefill(prompt(40, seed=2))
+    last = None
+    with pytest.raises(cb.CascadeError, match="full"):
+        for _ in range(64):
+            last = s.verify(np.array([1, 2, 3, 4], np.int32))
+            assert last.cache_len <= 48
+    assert last is not None and last.cache_len > 40
+    s.close()
+
+
 def test_utility_and_cost_breakdown(tiny):
     """CostBreakdown parts sum to total (expert_model_test.cpp:120-133) and
     the on-device utility equals emitted * t_base / total."""
