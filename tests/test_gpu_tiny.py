@@ -286,6 +286,54 @@ def test_kv_cache_bounds(tiny):
     s.close()
 
 
+def test_sessions_are_independent(tiny):
+    """One session per request, each owning its state (the reference runs
+    scenario cells in parallel, engine.hpp:427-459): two sessions on one
+    model, interleaved on one thread and run concurrently from two host
+    threads (each on its own stream), give exactly the results of running
+    each alone."""
+    import threading
+
+    shape, m, om = tiny
+    prompts = [prompt(30, seed=11), prompt(26, seed=12)]
+    ks = [3, 0, 8, 2, 5, 1]
+
+    def step(s, K):
+        o = s.verify(np.arange(1, K + 1, dtype=np.int32) * 5)
+        return (o.accepted, list(o.argmax[: K + 1]), o.cache_len, list(s.union_sizes()))
+
+    def alone(p):
+        s = cb.Session(m, max_ctx=256, k_max=8)
+        s.prefill(p)
+        out = [step(s, K) for K in ks]
+        s.close()
+        return out
+
+    ref = [alone(p) for p in prompts]
+    ss = [cb.Session(m, max_ctx=256, k_max=8) for _ in prompts]
+    for s, p in zip(ss, prompts):
+        s.prefill(p)
+    inter = [[], []]
+    for K in ks:
+        for i, s in enumerate(ss):
+            inter[i].append(step(s, K))
+    for s in ss:
+        s.close()
+    assert inter == ref
+
+    conc = [None, None]
+
+    def worker(i):
+        conc[i] = alone(prompts[i])
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert conc == ref
+
+
 def test_utility_and_cost_breakdown(tiny):
     """CostBreakdown parts sum to total (expert_model_test.cpp:120-133) and
     the on-device utility equals emitted * t_base / total."""
