@@ -53,7 +53,11 @@ struct RouteParams {
     unsigned long long* trace;
 };
 
-constexpr int kRowThreads = 512;            // route / combine: one CTA per token row
+#ifndef CASCADE_ROW_THREADS
+#define CASCADE_ROW_THREADS 512
+#endif
+constexpr int kRowThreads = CASCADE_ROW_THREADS;  // route / combine: one CTA per token row
+constexpr int kRowG = 8192 / (8 * kRowThreads);   // 8-column groups per thread (d <= 8192)
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
 
@@ -126,9 +130,9 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
             pre0[j] = i < p.d / 8 ? __ldg(w0 + i) : make_uint4(0, 0, 0, 0);
         }
     }
-    uint4 nw[2];  // norm weights of this thread's 8-column groups
+    uint4 nw[kRowG];  // norm weights of this thread's 8-column groups
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < kRowG; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         nw[j] = c < (p.d >> 3) ? __ldg(reinterpret_cast<const uint4*>(p.norm_w) + c) : make_uint4(0, 0, 0, 0);
     }
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     phase_stamp(p.trace, 0);
     // ---- norm: thread owns groups of 8 consecutive columns (wide loads/stores)
     const float4* x4 = reinterpret_cast<const float4*>(p.x + (long long)t * p.d);
-    constexpr int kG = 2;  // d <= 8192
+    constexpr int kG = kRowG;
     const int n8 = p.d >> 3;
     float4 xv[kG][2];
     float ss = 0.f;
@@ -365,7 +369,7 @@ struct CombineParams {
 __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombineParams p) {
     __shared__ float red[32];
     const int t = blockIdx.x;
-    constexpr int kG = 2;  // 8-column groups per thread
+    constexpr int kG = kRowG;  // 8-column groups per thread
     const int n8 = p.d >> 3;
     uint4 nw[kG];          // norm weights: constants, loaded before the dependency wait
 #pragma unroll
