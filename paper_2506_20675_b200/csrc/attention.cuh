@@ -163,10 +163,14 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         {
             constexpr int Q4 = HALF / 4;
             const int n_q = n_mt * 16 * Q4;
-            for (int e0 = 0; e0 < n_q; e0 += 4 * kAttnThreads) {
-                float4 qa[4], qb[4], ca[4], cb[4];
+#ifndef CASCADE_ATTN_QB
+#define CASCADE_ATTN_QB 4
+#endif
+            constexpr int kQB = CASCADE_ATTN_QB;  // query items per thread with loads in flight together
+            for (int e0 = 0; e0 < n_q; e0 += kQB * kAttnThreads) {
+                float4 qa[kQB], qb[kQB], ca[kQB], cb[kQB];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kQB; ++u) {
                     const int e = e0 + u * kAttnThreads + threadIdx.x;
                     const int r = e / Q4, i = (e - r * Q4) * 4;
                     qa[u] = qb[u] = ca[u] = cb[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kQB; ++u) {
                     const int e = e0 + u * kAttnThreads + threadIdx.x;
                     if (e >= n_q) continue;
                     const int r = e / Q4, i = (e - r * Q4) * 4;
