@@ -143,7 +143,9 @@ CASCADE_API int cascade_model_destroy(cascade_model* m);
 CASCADE_API int cascade_ep_unique_id(void* out, size_t n);
 
 /* One decode request: KV cache for max_ctx positions, CUDA graphs for every
- * in-flight width 1..k_max+1 captured lazily on first use. */
+ * in-flight width 1..k_max+1 captured lazily on first use.  The committed KV
+ * length never exceeds max_ctx: a committing step whose K+1 rows could take
+ * it past max_ctx is refused before launch (CASCADE_ERUNTIME, "full"). */
 CASCADE_API int cascade_session_create(cascade_model* m, int max_ctx, int k_max, void* stream,
                            cascade_session** out);
 CASCADE_API int cascade_session_destroy(cascade_session* s);
@@ -162,7 +164,9 @@ CASCADE_API int cascade_set_baseline(cascade_session* s, double t_base_ns);
 /* One verification step over the pending token plus `K` drafts (0 <= K <=
  * k_max): host buffers in, host struct out; the H2D of the drafts and the
  * D2H of the result are inside the captured graph.  `draft_ns` is the
- * caller's drafting time, folded into CostBreakdown.draft_time/total. */
+ * caller's drafting time, folded into CostBreakdown.draft_time/total.
+ * Precondition (checked before launch): cache_len + K + 1 <= max_ctx,
+ * else CASCADE_ERUNTIME and the session is unchanged. */
 CASCADE_API int cascade_verify(cascade_session* s, const int32_t* draft, int K, double draft_ns,
                    cascade_verify_out* out);
 
@@ -173,7 +177,13 @@ CASCADE_API int cascade_last_union_sizes(cascade_session* s, int32_t* out, int n
 /* Enqueue-only variant for timing: launches the step graph for width
  * K+1 on the session stream with inputs already resident, no host sync,
  * no result copy.  `commit` = 0 leaves the KV length unchanged so the same
- * context is re-verified every call. */
+ * context is re-verified every call.  The drafts are the session's current
+ * token slots (the last prefill chunk's tokens, or the last verify's
+ * drafts).  Step parameters live in one pinned slot per width; a call that
+ * changes its width's slot (commit flag, drafts, baseline) first waits for
+ * the stream, so an enqueued graph never sees a later call's parameters.
+ * A committing enqueue counts K+1 rows against max_ctx until the next
+ * cascade_sync, which reads the exact KV length back. */
 CASCADE_API int cascade_verify_enqueue(cascade_session* s, int K, int commit);
 CASCADE_API int cascade_sync(cascade_session* s);
 CASCADE_API void* cascade_session_stream(cascade_session* s);

@@ -625,7 +625,14 @@ struct cascade_session {
     bool own_stream = false;
     std::vector<void*> allocs;
     StepParams* d_params = nullptr;
+    // Pinned step parameters, one slot per width T: the step graph of width
+    // T copies slot T when it executes, so a slot is only rewritten after
+    // the stream drained (set_params) and enqueued graphs of other widths
+    // never see another call's parameters.
     StepParams* h_params = nullptr;
+    int32_t drafts[kMaxT] = {};  // token slots the next enqueue-only step verifies (last prefill chunk / verify)
+    int len_hi = 0;              // upper bound of the device KV length (exact after every host sync point)
+    int user_ctx = 0;            // max_ctx as created: committed KV length never exceeds it
     DevState* d_state = nullptr;
     cascade_verify_out* d_result = nullptr;
     cascade_verify_out* h_result = nullptr;
@@ -664,6 +671,7 @@ struct cascade_session {
     int attn_fused = 0;    // chunk combine inside the attention kernel (last item per KV head); A/B: the separate combine is as fast or faster
     int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
+    int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
     int* counters2 = nullptr;
     int* ffn_ready = nullptr;    // [slots] published gate/up super-tiles
@@ -818,6 +826,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     CK(cudaSetDevice(m->device));
     cascade_session* s = new cascade_session();
     s->m = m;
+    s->user_ctx = max_ctx;
     s->max_ctx = max_ctx + kMaxT;  // room for the in-flight rows
     s->k_max = k_max;
     s->max_chunks = (s->max_ctx + kChunk - 1) / kChunk + 1;
@@ -877,13 +886,13 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->kc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)) ||
         (rc = salloc(s, &s->vc, (size_t)D.L * D.KV * s->max_ctx * D.hd * 2, false)))
         return fail(rc);
-    cudaError_t e = cudaHostAlloc(&s->h_params, sizeof(StepParams), cudaHostAllocDefault);
+    cudaError_t e = cudaHostAlloc(&s->h_params, sizeof(StepParams) * (kMaxT + 1), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaHostAlloc(&s->h_result, sizeof(cascade_verify_out), cudaHostAllocDefault);
     if (e != cudaSuccess) {
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
     }
-    std::memset(s->h_params, 0, sizeof(StepParams));
+    std::memset(s->h_params, 0, sizeof(StepParams) * (kMaxT + 1));
     std::memset(s->h_result, 0, sizeof(cascade_verify_out));
     // Bulk L2 prefetch from latency-bound kernels measured slower on B200
     // (the issuing kernels stall on the bulk-prefetch queue); off by default.
@@ -899,6 +908,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_ATTN_FUSED")) s->attn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FUSED")) s->ffn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
+    if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
@@ -946,6 +956,19 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
         return fail(CASCADE_ECUDA);
     }
+    // The fused FFN needs its whole grid (2 CTAs per SM) resident at once.
+    // If this context cannot hold 2 per SM (a carveout override, an
+    // SM-limited context), use the two-launch path, which has no
+    // cross-CTA waits.
+    if (s->ffn_fused) {
+        int o1 = 0, o2 = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, expert_ffn_kernel<1>, kGemvThreads, gemv_smem_bytes<1>()) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, expert_ffn_kernel<2>, kGemvThreads, gemv_smem_bytes<2>()) != cudaSuccess) {
+            cudaGetLastError();
+            o1 = o2 = 0;
+        }
+        if ((long long)std::min(o1, o2) * m->num_sms < s->gemv_grid) s->ffn_fused = 0;
+    }
     if ((rc = calibrate_sm_rates(s))) return fail(rc);
     *out = s;
     return CASCADE_OK;
@@ -985,9 +1008,26 @@ static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaSt
     default: return launch_k(stream_gemv_kernel<NT, EPI_ARGMAX>, grid, kGemvThreads, sm, st, pdl, p);
     }
 }
-static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st) {
-    if (f.gu.T <= 8) return launch_k(expert_ffn_kernel<1>, grid, kGemvThreads, gemv_smem_bytes<1>(), st, true, f);
-    return launch_k(expert_ffn_kernel<2>, grid, kGemvThreads, gemv_smem_bytes<2>(), st, true, f);
+// The fused expert FFN's down phase waits on gate/up tiles produced by other
+// CTAs of the same grid, so the whole grid must be resident at once.  It is
+// launched cooperatively: the driver then guarantees co-residency (or fails
+// the launch with cudaErrorCooperativeLaunchTooLarge) even when other
+// sessions' kernels share the GPU, instead of relying on an idle device.
+static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemvThreads);
+    cfg.dynamicSmemBytes = f.gu.T <= 8 ? gemv_smem_bytes<1>() : gemv_smem_bytes<2>();
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = coop ? 2 : 1;
+    if (f.gu.T <= 8) return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<1>, f);
+    return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<2>, f);
 }
 static cudaError_t launch_gemv(int epi, const GemvParams& p, int grid, cudaStream_t st, bool pdl = true) {
     return p.T <= 8 ? launch_gemv_nt<1>(epi, p, grid, st, pdl) : launch_gemv_nt<2>(epi, p, grid, st, pdl);
@@ -1091,7 +1131,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         return s->trace + slot++;
     };
     const bool pf = s->prefetch;
-    CK(cudaMemcpyAsync(s->d_params, s->h_params, sizeof(StepParams), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->d_params, s->h_params + T, sizeof(StepParams), cudaMemcpyHostToDevice, st));
 
     EmbedParams ep{};
     ep.sp = s->d_params;
@@ -1346,7 +1386,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             // its own loads 2x slower (A/B, profiles/r01f/ab_ffn_trigger.txt)
             fp.gu.trigger = s->ffn_trigger;
             PB(6);
-            CK(launch_ffn(fp, s->gemv_grid, st));
+            CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop));
             PE();
             ++nk;
         } else {
@@ -1473,18 +1513,46 @@ static int run_step(cascade_session* s, int T) {
     return CASCADE_OK;
 }
 
+// Writes the step parameters of width T into slot T.  A graph already
+// enqueued for width T copies the slot when it runs, so a changed slot is
+// only written after the stream drained; an unchanged one is left alone
+// (back-to-back enqueues of the same step need no host sync).
+static int set_params(cascade_session* s, int T, int mode, int commit, const int32_t* tokens, double draft_ns) {
+    StepParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.mode = mode;
+    p.commit = commit;
+    p.T = T;
+    for (int i = 0; i < kMaxT; ++i) p.tokens[i] = tokens ? tokens[i] : 0;
+    p.t_base_ns = s->t_base_ns;
+    p.draft_ns = draft_ns;
+    if (std::memcmp(&p, s->h_params + T, sizeof(p)) != 0) {
+        CK(cudaStreamSynchronize(s->stream));
+        s->h_params[T] = p;
+    }
+    return CASCADE_OK;
+}
+
+// A committing step of width T must keep the committed KV length within
+// the session's max_ctx; checked before anything is launched.
+static int check_room(cascade_session* s, int T) {
+    if (s->len_hi + T > s->user_ctx)
+        return set_err(CASCADE_ERUNTIME, "session KV cache is full (max_ctx reached): cache_len " +
+                                             std::to_string(s->len_hi) + " + " + std::to_string(T) +
+                                             " in-flight rows > max_ctx " + std::to_string(s->user_ctx));
+    return CASCADE_OK;
+}
+
 extern "C" int cascade_profile_step(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n) {
     if (!s || !ns || !kind || !n || K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "bad arguments");
     CK(cudaSetDevice(s->m->device));
     CK(cudaStreamSynchronize(s->stream));
     const int T = K + 1;
-    s->h_params->mode = 0;
-    s->h_params->commit = 0;
-    s->h_params->T = T;
-    s->h_params->t_base_ns = s->t_base_ns;
+    int rc = set_params(s, T, 0, 0, s->drafts, 0.0);
+    if (rc) return rc;
     Prof prof;
     prof.st = s->stream;
-    int rc = enqueue_step(s, T, nullptr, &prof);
+    rc = enqueue_step(s, T, nullptr, &prof);
     if (rc) return rc;
     CK(cudaStreamSynchronize(s->stream));
     const int cnt = (int)prof.kind.size();
@@ -1505,11 +1573,9 @@ extern "C" int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t
     CK(cudaSetDevice(s->m->device));
     CK(cudaStreamSynchronize(s->stream));
     const int T = K + 1;
-    s->h_params->mode = 0;
-    s->h_params->commit = 0;
-    s->h_params->T = T;
-    s->h_params->t_base_ns = s->t_base_ns;
-    int rc = run_step(s, T);
+    int rc = set_params(s, T, 0, 0, s->drafts, 0.0);
+    if (rc) return rc;
+    rc = run_step(s, T);
     if (rc) return rc;
     CK(cudaStreamSynchronize(s->stream));
     const int cnt = s->trace_n[T];
@@ -1541,11 +1607,8 @@ extern "C" int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, 
     unsigned long long* base = s->trace;
     CK(cudaMemcpyToSymbol(g_cta_trace_base, &base, sizeof(base)));
     CK(cudaMemcpyToSymbol(g_cta_trace, &buf, sizeof(buf)));
-    s->h_params->mode = 0;
-    s->h_params->commit = 0;
-    s->h_params->T = T;
-    s->h_params->t_base_ns = s->t_base_ns;
-    rc = run_step(s, T);
+    rc = set_params(s, T, 0, 0, s->drafts, 0.0);
+    if (rc == CASCADE_OK) rc = run_step(s, T);
     cudaError_t e = cudaStreamSynchronize(s->stream);
     unsigned long long* null = nullptr;
     cudaMemcpyToSymbol(g_cta_trace, &null, sizeof(null));
@@ -1573,6 +1636,7 @@ extern "C" int cascade_session_reset(cascade_session* s) {
     CK(cudaStreamSynchronize(s->stream));
     CK(cudaMemset(s->d_state, 0, sizeof(DevState)));
     CK(cudaDeviceSynchronize());
+    s->len_hi = 0;
     return CASCADE_OK;
 }
 
@@ -1611,19 +1675,19 @@ extern "C" int cascade_prefill(cascade_session* s, const int32_t* prompt, int n)
     DevState ds;
     int rc = read_state(s, &ds);
     if (rc) return rc;
-    if (ds.cache_len + n - 1 + kMaxT > s->max_ctx) return set_err(CASCADE_EINVAL, "prefill exceeds max_ctx");
+    s->len_hi = ds.cache_len;
+    if (ds.cache_len + n - 1 > s->user_ctx) return set_err(CASCADE_EINVAL, "prefill exceeds max_ctx");
     for (int i = 0; i < n; ++i)
         if (prompt[i] < 0 || prompt[i] >= s->m->g.vocab) return set_err(CASCADE_EINVAL, "token id out of range");
     int pos = 0;
     while (pos < n - 1) {
         const int T = std::min(kMaxT, n - 1 - pos);
-        CK(cudaStreamSynchronize(s->stream));
-        std::memset(s->h_params, 0, sizeof(StepParams));
-        s->h_params->mode = 1;
-        s->h_params->commit = 1;
-        s->h_params->T = T;
-        for (int i = 0; i < T; ++i) s->h_params->tokens[i] = prompt[pos + i];
+        int32_t tok[kMaxT] = {};
+        for (int i = 0; i < T; ++i) tok[i] = prompt[pos + i];
+        if ((rc = set_params(s, T, 1, 1, tok, 0.0))) return rc;
+        std::memcpy(s->drafts, tok, sizeof(tok));
         if ((rc = run_step(s, T))) return rc;
+        s->len_hi += T;
         pos += T;
     }
     CK(cudaStreamSynchronize(s->stream));
@@ -1640,23 +1704,19 @@ extern "C" int cascade_verify(cascade_session* s, const int32_t* draft, int K, d
     for (int i = 0; i < K; ++i)
         if (draft[i] < 0 || draft[i] >= s->m->g.vocab) return set_err(CASCADE_EINVAL, "draft token out of range");
     CK(cudaSetDevice(s->m->device));
-    CK(cudaStreamSynchronize(s->stream));
     const int T = K + 1;
-    std::memset(s->h_params, 0, sizeof(StepParams));
-    s->h_params->mode = 0;
-    s->h_params->commit = 1;
-    s->h_params->T = T;
-    for (int i = 0; i < K; ++i) s->h_params->tokens[i + 1] = draft[i];
-    s->h_params->t_base_ns = s->t_base_ns;
-    s->h_params->draft_ns = draft_ns;
-    int rc = run_step(s, T);
+    int rc = check_room(s, T);
+    if (rc) return rc;
+    int32_t tok[kMaxT] = {};
+    for (int i = 0; i < K; ++i) tok[i + 1] = draft[i];
+    if ((rc = set_params(s, T, 0, 1, tok, draft_ns))) return rc;
+    std::memcpy(s->drafts, tok, sizeof(tok));
+    s->len_hi += T;
+    rc = run_step(s, T);
     if (rc) return rc;
     CK(cudaStreamSynchronize(s->stream));
     *out = *s->h_result;
-    if (out->cache_len + kMaxT > s->max_ctx) {
-        // the next step would not fit; report it now (the caller owns policy)
-        return set_err(CASCADE_ERUNTIME, "session KV cache is full (max_ctx reached)");
-    }
+    s->len_hi = out->cache_len;
     return CASCADE_OK;
 }
 
@@ -1664,17 +1724,20 @@ extern "C" int cascade_verify_enqueue(cascade_session* s, int K, int commit) {
     if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
     if (K < 0 || K > CASCADE_MAX_K) return set_err(CASCADE_EINVAL, "K out of range");
     const int T = K + 1;
-    s->h_params->mode = 0;
-    s->h_params->commit = commit ? 1 : 0;
-    s->h_params->T = T;
-    s->h_params->t_base_ns = s->t_base_ns;
-    int rc = run_step(s, T);
+    int rc = commit ? check_room(s, T) : CASCADE_OK;
+    if (rc) return rc;
+    if ((rc = set_params(s, T, 0, commit ? 1 : 0, s->drafts, 0.0))) return rc;
+    rc = run_step(s, T);
+    if (rc == CASCADE_OK && commit) s->len_hi += T;
     return rc;
 }
 
 extern "C" int cascade_sync(cascade_session* s) {
     if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
-    CK(cudaStreamSynchronize(s->stream));
+    DevState ds;
+    int rc = read_state(s, &ds);
+    if (rc) return rc;
+    s->len_hi = ds.cache_len;
     return CASCADE_OK;
 }
 

@@ -113,6 +113,10 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool staged = p.stage_w != 0 || C > 1;
     namespace cg = cooperative_groups;
+    // Cluster: every rank must have started before another rank writes its
+    // shared memory (DSMEM).  Arrive now, wait just before the first remote
+    // write; the wait overlaps the weight staging and the norm.
+    if (C > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     // ---- independent of the predecessor
     if (staged) {
         const uint4* src = reinterpret_cast<const uint4*>(p.router_w + (size_t)row_lo * p.d);
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
         acc = fmaf(b.w, __uint_as_float(w.w & 0xFFFF0000u), acc);
         return acc;
     };
+    if (C > 1) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     float* lg0 = C > 1 ? cg::this_cluster().map_shared_rank(s_lg, 0) : s_lg;  // rank 0's logits
     auto emit = [&](int e, float acc) {
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -267,11 +267,11 @@ def test_rejects_bad_requests(tiny):
 
 
 def test_kv_cache_bounds(tiny):
-    """The session's KV capacity is enforced: a prefill that would not leave
-    room for a full-width step is rejected (EINVAL), and the verify that
-    fills the cache reports it (ERUNTIME, after committing: the session
-    keeps kMaxT rows of headroom past max_ctx for the in-flight tokens)
-    instead of letting the next step write past the end."""
+    """The session's KV capacity is a precondition, checked before anything
+    is launched: a prefill beyond max_ctx is rejected (EINVAL); a committing
+    verify or enqueue whose K+1 in-flight rows could take the committed
+    length past max_ctx is refused (ERUNTIME, "full") and leaves the session
+    unchanged, so no step ever appends past the KV slab."""
     shape, m, om = tiny
     s = cb.Session(m, max_ctx=48, k_max=4)
     with pytest.raises(ValueError):
@@ -283,7 +283,28 @@ def test_kv_cache_bounds(tiny):
             last = s.verify(np.array([1, 2, 3, 4], np.int32))
             assert last.cache_len <= 48
     assert last is not None and last.cache_len > 40
+    # the refused step changed nothing; a narrower step that fits still runs
+    if last.cache_len + 1 <= 48:
+        o = s.verify(np.array([], np.int32))
+        assert o.cache_len == last.cache_len + 1
+    # enqueue-only committing steps are bounded the same way (upper bound
+    # T rows each until the next sync reads the exact length)
+    s2 = cb.Session(m, max_ctx=64, k_max=4)
+    s2.prefill(prompt(40, seed=2))
+    n_ok = 0
+    with pytest.raises(cb.CascadeError, match="full"):
+        for _ in range(64):
+            s2.enqueue(4, commit=True)
+            n_ok += 1
+    s2.sync()
+    assert n_ok == (64 - 39) // 5
+    try:
+        o = s2.verify(np.array([], np.int32))
+        assert 39 + n_ok < o.cache_len <= 64
+    except cb.CascadeError as e:  # every enqueued draft accepted: exactly full
+        assert "full" in str(e)
     s.close()
+    s2.close()
 
 
 def test_sessions_are_independent(tiny):
