@@ -276,6 +276,17 @@ typedef struct cascade_decode_cfg {
     const int32_t* replay_tokens;
     double replay_p;
     uint64_t replay_seed;
+    /* optional artifacts in the reference's formats (NULL = none):
+     *  telemetry_csv: IterationRecord CSV, header kTelemetryCsvHeader
+     *                 (report.hpp:123-138), one row per iteration;
+     *  trace_path:    acceptance trace "request_id,iter,k_offered,accepted"
+     *                 (trace.hpp:36,101-108), rows tagged `request_id`;
+     *                 trace_append = 1 adds this request to an existing file. */
+    const char* telemetry_csv;
+    const char* trace_path;
+    int64_t request_id;
+    int32_t trace_append;
+    int32_t reserved_cfg;
 } cascade_decode_cfg;
 
 CASCADE_API int cascade_decode(cascade_session* s, const int32_t* prompt, int n_prompt,
@@ -312,6 +323,39 @@ typedef struct cascade_cell_result {
 } cascade_cell_result;
 
 CASCADE_API int cascade_run_cell(cascade_session* s, const cascade_cell_cfg* cfg, cascade_cell_result* out);
+
+/* Geometry of the model a session runs (for host code above the ABI). */
+CASCADE_API int cascade_session_geometry(cascade_session* s, cascade_geometry* out);
+
+/* Device replay of an acceptance trace (the reference's `replay` command,
+ * tools/specsim.cpp:123-160, over engine.hpp replay_request 194-248 with the
+ * priced step replaced by real verification steps).  Every request of the
+ * trace (first-appearance order) is replayed under the policy of `cfg`
+ * (policy and ControllerConfig fields; -1 adaptive, 0 none, k static) on a
+ * random prompt of `prompt_len` tokens drawn from `seed`: each iteration's
+ * acceptance is the recorded one truncated to the offered k, forced on the
+ * real model by its own greedy continuation, and the costs are measured.
+ * Writes `out_csv` (NULL = none) in the reference's replay.csv format
+ * "request_id,iterations,tokens,total_time,t_base,tpot,etr,cost,utility";
+ * `total` receives the aggregate (requests, iterations, tokens, total_time,
+ * tpot, utility_hmean); `mismatches` the number of iterations where the
+ * device accepted a different count than the trace asked (0 expected). */
+CASCADE_API int cascade_replay_trace(cascade_session* s, const char* trace_path, const cascade_decode_cfg* cfg,
+                                     int32_t prompt_len, uint64_t seed, const char* out_csv,
+                                     cascade_cell_result* total, int64_t* mismatches);
+
+/* Device-backed scenario sweep: the reference's run_scenario (engine.hpp:
+ * 418-466) over verifier cells, reading the reference's scenario JSON
+ * (scenario.hpp schema; proj/fixtures/*.json load unchanged).  Cells are
+ * tasks x policies of the file on the loaded model (`model_name` in the
+ * report); `sessions[0..n_sessions)` are worker sessions, one per GPU (each
+ * on its own device's copy of the model), each running whole cells.
+ * tokens_per_cell > 0 overrides the file.  Writes out_dir/cells.csv and
+ * out_dir/summary.json in the reference's report formats (report.hpp).
+ * *n_cells = number of cells (failed cells are reported in the files). */
+CASCADE_API int cascade_run_scenario(cascade_session* const* sessions, int n_sessions, const char* scenario_json,
+                                     const char* out_dir, int64_t tokens_per_cell, int32_t prompt_len,
+                                     const char* model_name, int32_t* n_cells);
 
 /* Library build identity: "sm_100a" plus the git hash baked at build. */
 CASCADE_API const char* cascade_build_info(void);

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <optional>
 #include <random>
@@ -72,6 +73,17 @@ public:
         r.accepted = r.raw.accepted;
         r.emitted.assign(r.raw.tokens, r.raw.tokens + r.raw.emitted);
         return r;
+    }
+
+    // Drops the KV cache (the next prefill starts a new request).
+    void reset() { check_status(cascade_session_reset(s_)); }
+
+    void set_batch_invariant(bool on) { check_status(cascade_set_batch_invariant(s_, on ? 1 : 0)); }
+
+    int vocab() const {
+        cascade_geometry g{};
+        check_status(cascade_session_geometry(s_, &g));
+        return g.vocab;
     }
 
     cascade_session* session() const { return s_; }
@@ -150,7 +162,8 @@ struct GpuRunOptions {
     int k_limit = 8;                       // verifier K cap (session k_max)
     int baseline_probes = 4;               // K=0 steps that measure t_base for static/none policies
     std::optional<std::array<double, CASCADE_MAX_TOKENS>> injected_cost;  // k -> total_time
-    std::vector<TraceRecord>* trace = nullptr;  // records (0, iter, k_offered, accepted)
+    std::vector<TraceRecord>* trace = nullptr;  // records (trace_request_id, iter, k_offered, accepted)
+    long trace_request_id = 0;
 };
 
 // The reference request loop (engine.hpp:115-182) over the real verifier.
@@ -190,7 +203,7 @@ inline RequestMetrics run_request(Verifier& verifier, Drafter& drafter, const Po
             cost.expert_time = cost.total;
         }
         const IterationRecord rec = detail::make_record(iter, d, v.accepted, cost);
-        if (opt.trace) opt.trace->push_back({0, iter, static_cast<int>(drafts.size()), v.accepted});
+        if (opt.trace) opt.trace->push_back({opt.trace_request_id, iter, static_cast<int>(drafts.size()), v.accepted});
 
         if (ctl) {
             ctl->next_k(rec, analyzer);
@@ -259,20 +272,46 @@ struct NoDrafter {
     std::vector<int32_t> propose(const std::vector<int32_t>&, int) const { return {}; }
 };
 
-// One cell of the reference scenario sweep (engine.hpp run_cell / run_scenario,
-// 300-466) on the device: the task's request stream (profile mix, output
-// lengths, token budget) is drawn with the reference's policy-independent
-// seeds, every request gets a random prompt, its greedy continuation is
-// recorded with a K=0 decode, and the request is then decoded under the
+// The target's greedy continuation of `prompt` (n tokens, K=0 steps).  When
+// `t_base` is given it receives the mean device time of the first `probes`
+// of those K=0 steps: the no-speculation baseline of this request.
+inline std::vector<int32_t> greedy_continuation(Verifier& verifier, const std::vector<int32_t>& prompt, long n,
+                                                double* t_base = nullptr, int probes = 4) {
+    verifier.reset();
+    verifier.prefill(prompt);
+    std::vector<int32_t> out;
+    out.reserve(static_cast<std::size_t>(n));
+    double sum = 0.0;
+    int cnt = 0;
+    for (long i = 0; i < n; ++i) {
+        const VerifyResult r = verifier.verify({}, 0.0);
+        if (cnt < probes) {
+            sum += r.cost.total;
+            ++cnt;
+        }
+        out.push_back(r.emitted.at(0));
+    }
+    if (t_base) *t_base = cnt ? sum / cnt : 0.0;
+    verifier.reset();
+    return out;
+}
+
+// One cell of the reference scenario sweep (engine.hpp run_cell, 339-376) on
+// the device: the task's request stream (profile mix, output lengths, token
+// budget) is drawn from the workload seed `wseed` exactly as the reference
+// draws it, every request gets a random prompt, its greedy continuation is
+// recorded with K=0 steps, and the request is then decoded under the
 // policy with the profile-driven replay drafter.  Costs are the device's;
-// the aggregation is the reference's (tpot, ETR, cost, utility, harmonic mean).
-// The session must be batch-invariant so replayed drafts stay aligned.
-inline CellResult run_cell(Verifier& verifier, int vocab, const RequestStream& task, const Policy& policy,
-                           long tokens_per_cell, int prompt_len, uint64_t seed, const GpuRunOptions& opt = {}) {
+// the aggregation is the reference's (tpot, ETR, cost, utility, harmonic
+// mean).  The session is made batch-invariant so replayed drafts stay
+// aligned with the recorded continuation.
+inline CellResult run_cell_seeded(Verifier& verifier, int vocab, const RequestStream& task, const Policy& policy,
+                                  long tokens_per_cell, int prompt_len, std::uint64_t wseed,
+                                  const GpuRunOptions& opt = {}) {
     if (prompt_len < 1) throw std::invalid_argument("run_cell: prompt_len must be >= 1");
+    verifier.set_batch_invariant(true);
     CellResult cell;
     cell.policy = policy.label();
-    const std::uint64_t wseed = splitmix64(seed);
     Rng stream_rng(wseed);
     RequestStream stream = task;
     stream.max_tokens = tokens_per_cell;
@@ -285,14 +324,10 @@ inline CellResult run_cell(Verifier& verifier, int vocab, const RequestStream& t
         std::vector<int32_t> prompt(static_cast<std::size_t>(prompt_len));
         std::uniform_int_distribution<int32_t> tok(0, vocab - 1);
         for (int32_t& t : prompt) t = tok(prng);
-        std::vector<int32_t> truth_toks = prompt;
-        NoDrafter none_drafter;
-        check_status(cascade_session_reset(verifier.session()));
-        run_request(verifier, none_drafter, Policy::none(), truth_toks, len + CASCADE_MAX_TOKENS, opt);
-        std::vector<int32_t> truth(truth_toks.begin() + prompt_len, truth_toks.end());
+        std::vector<int32_t> truth = greedy_continuation(verifier, prompt, len + CASCADE_MAX_TOKENS);
         ProfileReplayDrafter drafter(std::move(truth), prompt_len, *profile, vocab, prng());
         std::vector<int32_t> toks = prompt;
-        check_status(cascade_session_reset(verifier.session()));
+        verifier.reset();
         RequestMetrics m = run_request(verifier, drafter, policy, toks, len, opt);
         ++cell.requests;
         cell.iterations += m.iterations;
@@ -308,6 +343,148 @@ inline CellResult run_cell(Verifier& verifier, int vocab, const RequestStream& t
     cell.utility = cell.etr / cell.cost;
     cell.utility_hmean = harmonic_mean(utils);
     return cell;
+}
+
+inline CellResult run_cell(Verifier& verifier, int vocab, const RequestStream& task, const Policy& policy,
+                           long tokens_per_cell, int prompt_len, uint64_t seed, const GpuRunOptions& opt = {}) {
+    return run_cell_seeded(verifier, vocab, task, policy, tokens_per_cell, prompt_len, splitmix64(seed), opt);
+}
+
+// The reference sweep (engine.hpp run_scenario, 418-466) over verifier-backed
+// cells.  The reference's cell thread pool (427-459) becomes one worker per
+// verifier session: sessions live on different GPUs (one per device, each
+// with its own weights), so cells run device-parallel; every worker pulls
+// the next cell index from a shared cursor and a failing cell is recorded
+// without stopping the sweep.  The models axis is the loaded device model
+// (`model_name`); tasks x policies are crossed as in the reference, with the
+// reference's policy-independent workload seeds (engine.hpp:355-357), so
+// every policy of a task faces the same requests.
+inline ScenarioReport run_scenario(const std::vector<Verifier*>& devices, const ScenarioConfig& cfg,
+                                   const std::string& model_name, int prompt_len, const GpuRunOptions& opt = {}) {
+    if (devices.empty()) throw std::invalid_argument("run_scenario: need at least one verifier session");
+    if (cfg.tasks.empty() || cfg.policies.empty())
+        throw std::invalid_argument("scenario needs at least one model, task, and policy");
+    for (const TaskSpec& t : cfg.tasks) t.stream.validate();
+    if (cfg.tokens_per_cell < 1) throw std::invalid_argument("tokens_per_cell must be >= 1");
+    ScenarioReport rep;
+    rep.name = cfg.name;
+    rep.seed = cfg.seed;
+    const std::size_t np = cfg.policies.size(), nt = cfg.tasks.size(), n = nt * np;
+    rep.cells.resize(n);
+    std::vector<int> vocab(devices.size());
+    for (std::size_t i = 0; i < devices.size(); ++i) vocab[i] = devices[i]->vocab();
+    std::atomic<std::size_t> cursor{0};
+    auto work = [&](std::size_t dev) {
+        for (std::size_t idx; (idx = cursor.fetch_add(1)) < n;) {
+            const std::size_t pi = idx % np, ti = idx / np;
+            CellResult& c = rep.cells[idx];
+            try {
+                const std::uint64_t wseed = splitmix64(cfg.seed ^ splitmix64(1 * 0x10001ull + (ti + 1) * 0x101ull));
+                c = run_cell_seeded(*devices[dev], vocab[dev], cfg.tasks[ti].stream, cfg.policies[pi],
+                                    cfg.tokens_per_cell, prompt_len, wseed, opt);
+            } catch (const std::exception& e) {
+                c = CellResult{};
+                c.failed = true;
+                c.error = e.what();
+            }
+            c.model_idx = 0;
+            c.task_idx = ti;
+            c.policy_idx = pi;
+            c.model = model_name;
+            c.task = cfg.tasks[ti].name;
+            c.policy = cfg.policies[pi].label();
+        }
+    };
+    if (devices.size() == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> pool;
+        for (std::size_t d = 0; d < devices.size(); ++d) pool.emplace_back(work, d);
+        for (std::thread& t : pool) t.join();
+    }
+    for (const Policy& p : cfg.policies)
+        if (p.kind == Policy::Kind::none) {
+            compare_policies(rep);
+            break;
+        }
+    return rep;
+}
+
+// Replays a recorded request on the device: the reference's replay loop
+// (engine.hpp replay_request, 194-248) with the priced step (227) swapped for
+// a real verification step.  The request spans exactly its recorded
+// iterations; each iteration's acceptance is the recorded one truncated to
+// the offered k (trace.hpp:69-74), and the costs are measured.  The drafts
+// force that acceptance on the real model: the first a = min(recorded, k)
+// drafts are the target's own greedy continuation and the next one is a
+// token the target does not pick, so the device's greedy check accepts
+// exactly a (the session is batch-invariant, so the continuation recorded
+// at K=0 is what every wider step computes).  Static and none policies run
+// the offered k on every recorded iteration, as the reference does; their
+// baseline is measured on the same request's K=0 continuation steps (the
+// reference takes an analytic one, engine.hpp:212).  `mismatches` counts
+// iterations where the device accepted something else (0 unless the model
+// or numerics changed under the trace).
+inline RequestMetrics replay_request(Verifier& verifier, const AcceptanceTrace& trace, long request_id,
+                                     const Policy& policy, const std::vector<int32_t>& prompt,
+                                     const GpuRunOptions& opt = {}, long* mismatches = nullptr) {
+    if (prompt.empty()) throw std::invalid_argument("replay_request: empty prompt");
+    const std::vector<const TraceRecord*> recorded = trace.iterations_of(request_id);
+    if (recorded.empty()) throw MissingRecordError(request_id, 0);
+    const int vocab = verifier.vocab();
+    verifier.set_batch_invariant(true);
+    long need = CASCADE_MAX_TOKENS;
+    for (const TraceRecord* r : recorded) need += r->accepted + 1;
+    double t_base = 0.0;
+    const std::vector<int32_t> truth = greedy_continuation(verifier, prompt, need, &t_base, opt.baseline_probes);
+    verifier.prefill(prompt);
+
+    UtilityAnalyzer analyzer(16);
+    std::optional<SpeculationController> ctl;
+    if (policy.kind == Policy::Kind::adaptive) {
+        ctl.emplace(policy.controller);
+    } else {
+        analyzer.set_baseline(t_base);
+        verifier.set_baseline(t_base);
+    }
+    std::vector<IterationRecord> telemetry;
+    long pos = 0, iter = 0, bad = 0;
+    using clock = std::chrono::steady_clock;
+    for (const TraceRecord* src : recorded) {
+        detail::Decision d = detail::decide(policy, ctl);
+        d.k = std::min(d.k, opt.k_limit);
+        const int want = std::min(src->accepted, d.k);
+        const auto t0 = clock::now();
+        std::vector<int32_t> drafts(truth.begin() + pos, truth.begin() + pos + d.k);
+        if (want < d.k) drafts[static_cast<std::size_t>(want)] = (drafts[static_cast<std::size_t>(want)] + 1) % vocab;
+        const double draft_ns = std::chrono::duration<double, std::nano>(clock::now() - t0).count();
+        const VerifyResult v = verifier.verify(drafts, policy.kind == Policy::Kind::none ? 0.0 : draft_ns);
+        if (v.accepted != want) ++bad;
+        CostBreakdown cost = v.cost;
+        if (opt.injected_cost) {
+            cost = CostBreakdown{};
+            cost.total = (*opt.injected_cost)[static_cast<std::size_t>(d.k)];
+            cost.expert_time = cost.total;
+        }
+        const IterationRecord rec = detail::make_record(iter, d, v.accepted, cost);
+        if (opt.trace) opt.trace->push_back({request_id, iter, static_cast<int>(drafts.size()), v.accepted});
+        if (ctl) {
+            ctl->next_k(rec, analyzer);
+            if (analyzer.baseline().valid()) verifier.set_baseline(analyzer.baseline().t_base);
+        } else {
+            analyzer.record(rec);
+        }
+        if (opt.engine.keep_telemetry) telemetry.push_back(rec);
+        pos += v.accepted + 1;
+        if (pos + CASCADE_MAX_TOKENS > static_cast<long>(truth.size())) break;  // device diverged past the record
+        ++iter;
+    }
+    if (mismatches) *mismatches = bad;
+    if (!analyzer.baseline().valid()) {
+        if (analyzer.pending_probe_count() > 0) analyzer.refresh_from_pending();
+        else throw MissingBaselineError{};
+    }
+    return detail::finalize_metrics(analyzer, std::move(telemetry));
 }
 
 }  // namespace specsim

@@ -17,9 +17,15 @@
 #include <thread>
 #include <vector>
 
+#include <cstdio>
+#include <sstream>
+#include <string>
+
 #include "landscape_harness.hpp"
 #include "specsim/engine.hpp"
 #include "specsim/expert_model.hpp"
+#include "specsim/report.hpp"
+#include "specsim/scenario.hpp"
 #include "specsim/trace.hpp"
 #include "specsim/utility.hpp"
 #include "specsim/workload.hpp"
@@ -241,6 +247,165 @@ int ref_window_utility(int window, double t_base, int n, const int32_t* k, const
         out[1] = an.window_cost();
         out[2] = an.window_utility();
         return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// ---- report / trace / scenario interop (f3, f4) --------------------------
+
+// AcceptanceTrace::load; out[4*i..] = request_id, iter, k_offered, accepted.
+// Returns the record count (<= cap), -1 on error.
+long ref_trace_load(const char* path, int64_t* out, long cap) {
+    try {
+        const AcceptanceTrace t = AcceptanceTrace::load(path);
+        long n = 0;
+        for (const TraceRecord& r : t.records()) {
+            if (n >= cap) break;
+            out[4 * n] = r.request_id;
+            out[4 * n + 1] = r.iter;
+            out[4 * n + 2] = r.k_offered;
+            out[4 * n + 3] = r.accepted;
+            ++n;
+        }
+        return n;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// replay_request of one request of a trace file (mixtral preset, ngram
+// draft, policy -1 adaptive / 0 none / k static, rng seed); out[8] as
+// ref_run_request; emitted[i] = tokens_emitted of iteration i.  Returns the
+// iteration count, -1 on error.
+long ref_trace_replay_request(const char* path, long request_id, int policy, uint64_t seed, double* out,
+                              int32_t* emitted, long cap) {
+    try {
+        const AcceptanceTrace t = AcceptanceTrace::load(path);
+        Policy pol = policy < 0 ? Policy::adaptive({}) : (policy == 0 ? Policy::none() : Policy::static_k(policy));
+        Rng rng(seed);
+        EngineOptions opts;
+        opts.keep_telemetry = true;
+        const RequestMetrics m =
+            replay_request(t, request_id, pol, expert_preset("mixtral"), draft_preset("ngram"), rng, opts);
+        out[0] = (double)m.tokens;
+        out[1] = (double)m.iterations;
+        out[2] = m.total_time;
+        out[3] = m.t_base;
+        out[4] = m.tpot;
+        out[5] = m.etr;
+        out[6] = m.cost;
+        out[7] = m.utility;
+        long n = 0;
+        for (const IterationRecord& r : m.telemetry)
+            if (n < cap) emitted[n++] = r.tokens_emitted;
+        return (long)m.telemetry.size();
+    } catch (...) {
+        return -1;
+    }
+}
+
+// write_telemetry_csv of n records given as rows of 9 doubles
+// (iter, k, tokens, draft, verify, sampling, total, tag, trial).
+int ref_write_telemetry(const char* path, int n, const double* rows) {
+    try {
+        std::vector<IterationRecord> recs(n);
+        for (int i = 0; i < n; ++i) {
+            const double* r = rows + 9 * i;
+            recs[i].iter_index = (long)r[0];
+            recs[i].k_used = (int)r[1];
+            recs[i].tokens_emitted = (int)r[2];
+            recs[i].draft_time = r[3];
+            recs[i].verify_time = r[4];
+            recs[i].sampling_time = r[5];
+            recs[i].total_time = r[6];
+            recs[i].tag = (PhaseTag)(int)r[7];
+            recs[i].trial_no = (int)r[8];
+        }
+        write_telemetry_csv(recs, path);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// Runs the simulated scenario sweep of a scenario file (tokens override >0)
+// and writes cells.csv + summary.json (without the timestamp line) to dir.
+int ref_scenario_report(const char* scenario, long tokens, const char* dir) {
+    try {
+        ScenarioConfig cfg = load_scenario(scenario);
+        if (tokens > 0) cfg.tokens_per_cell = tokens;
+        const ScenarioReport rep = run_scenario(cfg);
+        write_cells_csv(rep, std::string(dir) + "/cells.csv");
+        std::ofstream out(std::string(dir) + "/summary.json");
+        out << summary_json(rep, false).dump(2) << "\n";
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+// load_cells_csv; out[3*i..] = requests, tokens, utility; returns the row
+// count (<= cap) or -1.
+long ref_load_cells(const char* path, double* out, long cap) {
+    try {
+        const std::vector<CellResult> cells = load_cells_csv(path);
+        long n = 0;
+        for (const CellResult& c : cells) {
+            if (n >= cap) break;
+            out[3 * n] = (double)c.requests;
+            out[3 * n + 1] = (double)c.tokens;
+            out[3 * n + 2] = c.utility;
+            ++n;
+        }
+        return (long)cells.size();
+    } catch (...) {
+        return -1;
+    }
+}
+
+// A canonical text digest of a parsed scenario (for parser parity).
+// Returns the digest length (copied into buf, NUL-terminated) or -1.
+long ref_scenario_digest(const char* path, char* buf, long n) {
+    try {
+        const ScenarioConfig c = load_scenario(path);
+        std::ostringstream o;
+        o.precision(17);
+        o << c.name << '|' << c.seed << '|' << c.seed_in_file << '|' << c.tokens_per_cell << '|' << c.jobs << '|'
+          << (int)c.draft.kind << ',' << c.draft.per_k_overhead << ',' << c.draft.sampling_overhead << ','
+          << c.draft.always_on_overhead << "\n";
+        for (const ExpertConfig& m : c.models)
+            o << "M " << m.name << ',' << m.num_layers << ',' << m.experts_per_layer << ',' << m.top_k << ','
+              << m.shared_experts << ',' << m.affinity << ',' << m.baseline_iter_time << ',' << m.attention_fraction
+              << "\n";
+        for (const TaskSpec& t : c.tasks) {
+            o << "T " << t.name << "\n";
+            for (const auto& [p, share] : t.stream.mix) {
+                o << "  P " << p.name << ',' << share << ',' << (int)p.transition << ',' << p.output_len.lo << ','
+                  << p.output_len.hi << ',' << (p.expert_affinity ? *p.expert_affinity : -1.0) << "\n";
+                for (const AcceptancePhase& ph : p.phases)
+                    o << "    " << ph.per_token_accept_prob << ',' << ph.mean_duration << ','
+                      << (ph.affinity_override ? *ph.affinity_override : -1.0) << "\n";
+                for (const auto& row : p.transition_matrix) {
+                    o << "    R";
+                    for (double v : row) o << ' ' << v;
+                    o << "\n";
+                }
+            }
+        }
+        for (const Policy& p : c.policies) {
+            const ControllerConfig& k = p.controller;
+            o << "P " << p.label() << ',' << k.t_trial << ',' << k.max_trials << ',' << k.s_set << ',' << k.s_cap
+              << ',' << k.k_max << ',' << k.k_start << ',' << k.convergence_band << ',' << k.baseline_refresh_interval
+              << ',' << k.baseline_probe_len << ',' << k.backoff_enabled << "\n";
+        }
+        const std::string d = o.str();
+        if (buf && n > 0) {
+            const long c2 = (long)d.size() < n - 1 ? (long)d.size() : n - 1;
+            std::memcpy(buf, d.data(), (size_t)c2);
+            buf[c2] = 0;
+        }
+        return (long)d.size();
     } catch (...) {
         return -1;
     }

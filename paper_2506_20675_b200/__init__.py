@@ -113,6 +113,11 @@ class DecodeCfg(ctypes.Structure):
         ("replay_tokens", ctypes.POINTER(ctypes.c_int32)),
         ("replay_p", ctypes.c_double),
         ("replay_seed", ctypes.c_uint64),
+        ("telemetry_csv", ctypes.c_char_p),
+        ("trace_path", ctypes.c_char_p),
+        ("request_id", ctypes.c_int64),
+        ("trace_append", ctypes.c_int32),
+        ("reserved_cfg", ctypes.c_int32),
     ]
 
 
@@ -298,6 +303,17 @@ def lib() -> ctypes.CDLL:
             ],
         ),
         "cascade_build_info": (ctypes.c_char_p, []),
+        "cascade_session_geometry": (ctypes.c_int, [P, ctypes.POINTER(Geometry)]),
+        "cascade_replay_trace": (
+            ctypes.c_int,
+            [P, ctypes.c_char_p, ctypes.POINTER(DecodeCfg), i32, u64, ctypes.c_char_p, ctypes.POINTER(CellResult),
+             ctypes.POINTER(i64)],
+        ),
+        "cascade_run_scenario": (
+            ctypes.c_int,
+            [ctypes.POINTER(P), ctypes.c_int, ctypes.c_char_p, ctypes.c_char_p, i64, i32, ctypes.c_char_p,
+             ctypes.POINTER(i32)],
+        ),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -528,7 +544,14 @@ class Session:
         _check(lib().cascade_read_kv(self.h, layer, which, length, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16))))
         return out
 
-    def decode(self, prompt, cfg: DecodeCfg, telemetry_cap: int = 0):
+    def decode(self, prompt, cfg: DecodeCfg, telemetry_cap: int = 0, telemetry_csv: Optional[str] = None,
+               trace_path: Optional[str] = None, request_id: int = 0, trace_append: bool = False):
+        """cascade_decode; optionally writes the IterationRecord CSV (report.hpp
+        telemetry format) and the acceptance trace (trace.hpp format)."""
+        cfg.telemetry_csv = telemetry_csv.encode() if telemetry_csv else None
+        cfg.trace_path = trace_path.encode() if trace_path else None
+        cfg.request_id = request_id
+        cfg.trace_append = 1 if trace_append else 0
         p = np.ascontiguousarray(prompt, np.int32)
         out = np.zeros(cfg.max_new + MAX_TOKENS, np.int32)
         n_out = ctypes.c_int32()
@@ -538,6 +561,35 @@ class Session:
                                     tel.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if telemetry_cap else None,
                                     telemetry_cap, ctypes.byref(n_it)))
         return out[: n_out.value], tel[: min(n_it.value, telemetry_cap)], n_it.value
+
+
+def _cell_dict(r: CellResult) -> dict:
+    return {n: getattr(r, n) for n, _ in CellResult._fields_}
+
+
+def replay_trace(session: "Session", trace_path: str, policy: int = -1, prompt_len: int = 32, seed: int = 1,
+                 out_csv: Optional[str] = None, **controller) -> dict:
+    """Device replay of an acceptance trace (cascade_replay_trace): recorded
+    acceptance (truncated to the offered k), measured costs."""
+    c = decode_cfg(policy=policy, **controller)
+    tot = CellResult()
+    mism = ctypes.c_int64()
+    _check(lib().cascade_replay_trace(session.h, trace_path.encode(), ctypes.byref(c), prompt_len, seed,
+                                      out_csv.encode() if out_csv else None, ctypes.byref(tot), ctypes.byref(mism)))
+    d = _cell_dict(tot)
+    d["mismatches"] = mism.value
+    return d
+
+
+def run_scenario_device(sessions, scenario_json: str, out_dir: str, tokens_per_cell: int = 0, prompt_len: int = 32,
+                        model_name: str = "device") -> int:
+    """Device-backed scenario sweep (cascade_run_scenario): one worker per
+    session (one per GPU); writes out_dir/cells.csv and summary.json."""
+    arr = (ctypes.c_void_p * len(sessions))(*[s.h.value for s in sessions])
+    n = ctypes.c_int32()
+    _check(lib().cascade_run_scenario(arr, len(sessions), scenario_json.encode(), out_dir.encode(), tokens_per_cell,
+                                      prompt_len, model_name.encode(), ctypes.byref(n)))
+    return n.value
 
 
 def decode_cfg(policy: int = -1, max_new: int = 128, ngram_n: int = 3, **controller) -> DecodeCfg:

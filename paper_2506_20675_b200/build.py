@@ -15,6 +15,11 @@ PKG = os.path.join(ROOT, "paper_2506_20675_b200")
 CSRC = os.path.join(PKG, "csrc")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# nlohmann/json (header-only; the parser the reference's scenario/report code
+# uses), shipped in the image with cudnn_frontend.  Compile-time only.
+JSON_INC = os.environ.get("CASCADE_JSON_INC") or os.path.join(
+    sys.prefix, "lib", f"python{sys.version_info.major}.{sys.version_info.minor}", "site-packages", "include",
+    "cudnn_frontend", "thirdparty", "nlohmann")
 
 
 def _git_hash() -> str:
@@ -43,7 +48,7 @@ def build_cascade(force: bool = False, verbose: bool = False) -> str:
         deps += [os.path.join(spec, f) for f in os.listdir(spec)]
     if not force and not _newer(out, deps):
         return out
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", f"-I{inc}", f"-I{CSRC}", "-Xcompiler", "-fPIC",
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", f"-I{inc}", f"-I{CSRC}", f"-I{JSON_INC}", "-Xcompiler", "-fPIC",
            "-Xcompiler", "-fvisibility=hidden", f'-DCASCADE_GIT="{_git_hash()}"', "-shared", "-o", out, *srcs,
            "-ldl"]
     if verbose:

@@ -975,6 +975,11 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
 }
 
 extern "C" void* cascade_session_stream(cascade_session* s) { return s ? (void*)s->stream : nullptr; }
+extern "C" int cascade_session_geometry(cascade_session* s, cascade_geometry* out) {
+    if (!s || !out) return set_err(CASCADE_EINVAL, "session/out is NULL");
+    *out = s->m->g;
+    return CASCADE_OK;
+}
 extern "C" int cascade_internal_vocab(const cascade_session* s) { return s ? s->m->g.vocab : 0; }
 
 // ------------------------------------------------------------ step enqueue

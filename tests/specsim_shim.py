@@ -43,6 +43,13 @@ class Shim:
                                     ctypes.c_uint64, DP]),
             "ref_window_utility": (c, [c, ctypes.c_double, c, I32P, I32P, DP, I32P, DP]),
             "ref_controller_replay": (c, [I32P, ctypes.c_double, c, I32P, DP, I32P, I32P]),
+            "ref_trace_load": (ctypes.c_long, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_long]),
+            "ref_trace_replay_request": (ctypes.c_long, [ctypes.c_char_p, ctypes.c_long, c, ctypes.c_uint64, DP,
+                                                         I32P, ctypes.c_long]),
+            "ref_write_telemetry": (c, [ctypes.c_char_p, c, DP]),
+            "ref_scenario_report": (c, [ctypes.c_char_p, ctypes.c_long, ctypes.c_char_p]),
+            "ref_load_cells": (ctypes.c_long, [ctypes.c_char_p, DP, ctypes.c_long]),
+            "ref_scenario_digest": (ctypes.c_long, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_long]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)
@@ -126,6 +133,39 @@ class Shim:
                                             total.ctypes.data_as(DP), k.ctypes.data_as(I32P),
                                             tg.ctypes.data_as(I32P)) == 0
         return k, tg
+
+    # ---- report / trace / scenario interop
+    def trace_load(self, path, cap=100000):
+        out = np.zeros((cap, 4), np.int64)
+        n = self.L.ref_trace_load(str(path).encode(), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), cap)
+        assert n >= 0, f"trace load failed: {path}"
+        return out[:n]
+
+    def trace_replay_request(self, path, request_id, policy, seed=1, cap=100000):
+        out = np.zeros(8)
+        em = np.zeros(cap, np.int32)
+        n = self.L.ref_trace_replay_request(str(path).encode(), request_id, policy, seed, out.ctypes.data_as(DP),
+                                            em.ctypes.data_as(I32P), cap)
+        assert n >= 0
+        return out, em[:n]
+
+    def write_telemetry(self, path, rows):
+        rows = np.ascontiguousarray(rows, np.float64)
+        assert self.L.ref_write_telemetry(str(path).encode(), len(rows), rows.ctypes.data_as(DP)) == 0
+
+    def scenario_report(self, scenario, tokens, out_dir):
+        assert self.L.ref_scenario_report(str(scenario).encode(), tokens, str(out_dir).encode()) == 0
+
+    def load_cells(self, path, cap=4096):
+        out = np.zeros((cap, 3))
+        n = self.L.ref_load_cells(str(path).encode(), out.ctypes.data_as(DP), cap)
+        assert n >= 0, f"load_cells failed: {path}"
+        return out[:n]
+
+    def scenario_digest(self, path):
+        buf = ctypes.create_string_buffer(1 << 16)
+        n = self.L.ref_scenario_digest(str(path).encode(), buf, 1 << 16)
+        return None if n < 0 else buf.value.decode()
 
 
 DEFAULT_CFG = {"t_trial": 4, "max_trials": 4, "s_set": 16, "s_cap": 256, "k_max": 3, "k_start": 3, "refresh": 100,
