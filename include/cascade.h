@@ -205,10 +205,12 @@ CASCADE_API int cascade_profile_step(cascade_session* s, int K, double* ns, int3
 CASCADE_API int cascade_step_trace(cascade_session* s, int K, double* ns, int32_t* kind, int cap, int* n);
 
 /* Per-CTA timeline of one captured step of width K+1 (diagnostic, commit =
- * 0): out[(i * 512 + cta) * 2 + {0, 1}] = %globaltimer (ns) when CTA `cta`
- * of launch i started (after its dependency wait) and when it exited; 0
- * for CTAs that do not exist (cta >= 512 is not recorded).  kind[i] as in
- * cascade_profile_step; *n_slots = launches (<= cap_slots). */
+ * 0): out[(i * 512 + cta) * 4 + {0, 1}] = %globaltimer (ns) when CTA `cta`
+ * of launch i started (after its dependency wait) and when it exited;
+ * {2, 3} = optional phase stamps (expert FFN: gate/up range done, first
+ * down-phase readiness wait released); 0 for CTAs / stamps that do not
+ * exist (cta >= 496 is not recorded).  kind[i] as in cascade_profile_step;
+ * *n_slots = launches (<= cap_slots). */
 CASCADE_API int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, int32_t* kind, int cap_slots,
                                        int* n_slots);
 

@@ -196,7 +196,7 @@ class ModelShape:
         expert = 3 * d * f * 2
         out = {"experts": 0, "dense": 0, "kv": 0, "head": 0}
         for u in union_sizes:
-            u = int(u)
+            u = float(u)  # a mean U over draws is fractional: never truncate it
             out["experts"] += (u + self.shared_experts) * expert
             out["dense"] += (d * (hq + 2 * kvd) + hq * d) * 2 + (self.experts_per_layer + self.shared_gate) * d * 2 + 2 * d * 2
             out["kv"] += ctx * 2 * kvd * 2 + T * 2 * kvd * 2
@@ -486,10 +486,10 @@ class Session:
         return ns[: n.value], kind[: n.value]
 
     def cta_trace(self, K: int):
-        """Per-CTA (start, exit) globaltimer stamps of one captured step:
-        array [launches][512][2] (ns, 0 = no such CTA) and the launch classes."""
+        """Per-CTA (start, exit, phase a, phase b) globaltimer stamps of one captured
+        step: array [launches][512][4] (ns, 0 = none) and the launch classes."""
         cap = 64 * self.model.shape.num_layers + 16
-        out = np.zeros((cap, 512, 2), np.uint64)
+        out = np.zeros((cap, 512, 4), np.uint64)
         kind = np.zeros(cap, np.int32)
         n = ctypes.c_int()
         _check(lib().cascade_step_cta_trace(self.h, K, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),

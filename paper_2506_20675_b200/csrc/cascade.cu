@@ -687,6 +687,8 @@ struct cascade_session {
     int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
     int o_cluster = 0;     // same for the O projection
+    int dn_prefetch = 8;   // fused FFN: k-steps of each warp's down range prefetched to L2 during the readiness wait (A/B: -1.5% at K=0)
+    int min_seg = 8;       // k-steps per warp below which the stream-K split uses fewer pieces than CTAs
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -878,7 +880,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         (rc = salloc(s, &s->ycontrib, (size_t)kMaxT * (D.k + D.S) * D.d * 4)) ||
         (rc = salloc(s, &s->partial, (size_t)std::max<long long>(workers, (long long)nslots * s->gemv_grid) * 2 * kTPW * 2 * 32 * 16, false)) ||
         (rc = salloc(s, &s->partial2, (size_t)std::max<long long>(workers, (long long)nslots * s->gemv_grid) * 2 * kTPW * 2 * 32 * 16, false)) ||
-        (rc = salloc(s, &s->counters2, (size_t)max_units * 4)) || (rc = salloc(s, &s->ffn_ready, (size_t)(nslots + 1) * 4)) ||
+        (rc = salloc(s, &s->counters2, (size_t)max_units * 4)) || (rc = salloc(s, &s->ffn_ready, (size_t)(nslots + 1) * kReadyStride * 4)) ||
         (rc = salloc(s, &s->counters, (size_t)max_units * 4)) || (rc = salloc(s, &s->attn_arrive, (size_t)D.KV * 4)) || (rc = salloc(s, &s->keys, kMaxT * 8)) ||
         (rc = salloc(s, &s->stamps, (size_t)(2 * D.L + 4) * 8)) || (rc = salloc(s, &s->tokens_used, kMaxT * 4)) ||
         (rc = salloc(s, &s->rope, (size_t)kMaxT * (D.hd / 2) * sizeof(float2))) ||
@@ -909,6 +911,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_FUSED")) s->ffn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
+    if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
+    if (const char* v = getenv("CASCADE_DN_PF")) s->dn_prefetch = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
@@ -1085,7 +1089,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
 static GemvParams gemv_base(cascade_session* s, int T) {
     GemvParams p{};
     p.T = T;
-    p.min_seg = 8;
+    p.min_seg = s->min_seg;
     p.partial = s->partial;
     p.counters = s->counters;
     p.invariant = s->invariant;
@@ -1384,6 +1388,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             fp.gu = gu;
             fp.dn = dn;
             fp.dn.partial = s->partial2;
+            fp.dn.trace = gu.trace;  // per-CTA phase stamps of the down phase (diagnostic trace only)
+            fp.dn.l2_prologue = s->dn_prefetch;
             fp.dn.counters = s->counters2;
             fp.ready = s->ffn_ready;
             fp.n_st_gu = gu.n_st;
@@ -1605,7 +1611,7 @@ extern "C" int cascade_step_cta_trace(cascade_session* s, int K, uint64_t* out, 
     if (rc) return rc;
     const int cnt = s->trace_n[T];
     if (cnt > cap_slots) return set_err(CASCADE_EINVAL, "trace buffer too small: need " + std::to_string(cnt));
-    const size_t bytes = (size_t)cnt * kCtaTraceCap * 2 * 8;
+    const size_t bytes = (size_t)cnt * kCtaTraceCap * kCtaRec * 8;
     unsigned long long* buf = nullptr;
     CK(cudaMalloc(&buf, bytes));
     CK(cudaMemset(buf, 0, bytes));

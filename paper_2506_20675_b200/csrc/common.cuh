@@ -28,6 +28,7 @@ namespace cascade {
 constexpr int kTPW = 4;                 // 16-row tiles per super-tile (per warp)
 constexpr int kSTRows = 16 * kTPW;      // 64 rows per super-tile
 constexpr int kMaxT = 16;               // tokens in flight (two n8 tiles)
+constexpr int kReadyStride = 32;        // ints: one 128-byte line per fused-FFN slot readiness counter
 
 __device__ __forceinline__ uint64_t globaltimer_raw() {
     uint64_t t;
@@ -73,9 +74,11 @@ __device__ __forceinline__ void prefetch_l2(const void* base, unsigned long long
 
 // Per-CTA timeline (diagnostic, cascade_step_cta_trace): when g_cta_trace
 // is set, every CTA records the globaltimer at its start (after
-// griddepcontrol.wait) and at its exit, at [(slot * kCtaTraceCap + cta) * 2].
+// griddepcontrol.wait) and at its exit, at [(slot * kCtaTraceCap + cta) * kCtaRec + {0, 1}];
+// records 2..3 hold optional per-CTA phase stamps (cta_phase).
 // Null in normal runs: one predicated global load per kernel.
 constexpr int kCtaTraceCap = 512;
+constexpr int kCtaRec = 4;  // u64 per CTA record: start, exit, phase a, phase b
 constexpr int kPhaseBase = 496;  // CTA records >= this hold CTA 0's phase stamps
 __device__ unsigned long long* g_cta_trace = nullptr;
 __device__ unsigned long long* g_cta_trace_base = nullptr;  // the session's trace slot 0
@@ -85,7 +88,7 @@ __device__ __forceinline__ unsigned long long* cta_trace_slot(unsigned long long
     if (buf == nullptr || slot == nullptr) return nullptr;
     const long long cta = (long long)blockIdx.y * gridDim.x + blockIdx.x;
     if (cta >= kPhaseBase) return nullptr;
-    return buf + ((slot - g_cta_trace_base) * kCtaTraceCap + cta) * 2;
+    return buf + ((slot - g_cta_trace_base) * kCtaTraceCap + cta) * kCtaRec;
 }
 
 // per-kernel start stamp for in-graph tracing (block 0, thread 0)
@@ -114,7 +117,13 @@ struct CtaExitStamp {
 __device__ __forceinline__ void phase_stamp(unsigned long long* slot, int i) {
     unsigned long long* buf = g_cta_trace;
     if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
-    buf[(slot - g_cta_trace_base) * kCtaTraceCap * 2 + kPhaseBase * 2 + i] = globaltimer_raw();
+    buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = globaltimer_raw();
+}
+// Per-CTA phase stamp (diagnostic): record `which` (2 or 3) of this CTA
+// keeps the latest stamp of any warp that reports it.
+__device__ __forceinline__ void cta_phase(unsigned long long* slot, int which) {
+    unsigned long long* c = cta_trace_slot(slot);
+    if (c != nullptr && (threadIdx.x & 31) == 0) atomicMax(c + which, globaltimer_raw());
 }
 #define CTA_TRACE(slot)   \
     trace_start(slot);    \

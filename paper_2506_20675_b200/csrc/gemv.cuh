@@ -628,6 +628,17 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
     uint4 a[kUnroll][kTPW];
     bool pre = false;
     unsigned long long ready_mask[WAIT ? (kMaxSlots + 63) / 64 : 1] = {};
+    bool waited = false;
+    // CTA-wide readiness: one warp polls a slot's global counter (the first
+    // to need it claims s_poll[slot]); the others watch the shared bit.  A
+    // poll per warp on one counter line (2368 warps) delayed the release by
+    // microseconds behind the publishing atomics.
+    __shared__ unsigned int s_ready_bits[(kMaxSlots + 31) / 32];
+    __shared__ int s_poll[kMaxSlots];
+    if constexpr (WAIT) {
+        for (int i = threadIdx.x; i < (kMaxSlots + 31) / 32; i += blockDim.x) s_ready_bits[i] = 0u;
+        for (int i = threadIdx.x; i < kMaxSlots; i += blockDim.x) s_poll[i] = 0;
+    }
     (void)kSlot;
     const int U = routed ? un.count : (p.count ? *p.count : p.n_blocks);
     const long long per_block = (long long)p.n_st * p.n_ks * (p.invariant ? 1 : U);
@@ -652,6 +663,31 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
             seg_unit[warp][1] = -1;
         }
         __syncwarp();
+        if constexpr (WAIT) {
+            // Down phase: the weights do not depend on the gate/up results, so
+            // the first p.l2_prologue k-steps of this warp's range stream into
+            // L2 while the CTA waits for its slots' readiness.
+            if (p.l2_prologue > 0 && item == wi && lane == 0) {
+                const long long pf_to = wlo + p.l2_prologue < whi ? wlo + p.l2_prologue : whi;
+                for (long long q = wlo; q < pf_to;) {
+                    const long long unit = q / p.n_ks;
+                    const int ks = (int)(q - unit * p.n_ks);
+                    long long n = p.n_ks - ks;
+                    if (pf_to - q < n) n = pf_to - q;
+                    const int bl = (int)(unit / p.n_st);
+                    const int st = (int)(unit - (long long)bl * p.n_st);
+                    const char* src = reinterpret_cast<const char*>(
+                        p.W + (long long)un.list[bl] * p.w_block_stride + ((long long)st * p.n_ks + ks) * (kTPW * 32));
+                    const unsigned long long bytes = (unsigned long long)n * kTPW * 32 * 16;
+                    for (unsigned long long off = 0; off < bytes; off += 65536) {
+                        const unsigned long long sz = bytes - off < 65536 ? bytes - off : 65536;
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"((uint32_t)sz)
+                                     : "memory");
+                    }
+                    q += n;
+                }
+            }
+        }
 
         long long pos = wlo;
         while (pos < whi) {
@@ -665,16 +701,32 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
             if constexpr (WAIT) {
                 if (!((ready_mask[bl >> 6] >> (bl & 63)) & 1ull)) {
                     if (lane == 0) {
+                        volatile unsigned int* bits = s_ready_bits;
+                        const unsigned int bit = 1u << (bl & 31);
+                        const bool poller = !(bits[bl >> 5] & bit) && atomicCAS(&s_poll[bl], 0, 1) == 0;
                         long long spins = 0;
-                        int v;
                         for (;;) {
-                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready + bl) : "memory");
-                            if (v >= target) break;
-                            if (++spins > (1ll << 22)) __trap();  // a lost producer must not hang the GPU (~seconds)
-                            __nanosleep(64);
+                            if (bits[bl >> 5] & bit) break;
+                            if (poller) {
+                                int v;
+                                asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
+                                             : "=r"(v)
+                                             : "l"(ready + (long long)bl * kReadyStride)
+                                             : "memory");
+                                if (v >= target) {
+                                    __threadfence_block();
+                                    atomicOr(&s_ready_bits[bl >> 5], bit);
+                                    break;
+                                }
+                            }
+                            if (++spins > (1ll << 24)) __trap();  // a lost producer must not hang the GPU (~seconds)
+                            __nanosleep(poller ? 32 : 64);
                         }
+                        __threadfence_block();
                     }
                     __syncwarp();
+                    if (!waited) cta_phase(p.trace, 3);  // first readiness wait of this warp released
+                    waited = true;
                     ready_mask[bl >> 6] |= 1ull << (bl & 63);
                 }
             }
@@ -812,10 +864,11 @@ __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f
     __syncthreads();
     if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
     ffn_phase<NT, EPI_GATEUP, false>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
+    cta_phase(f.gu.trace, 2);  // gate/up range of this CTA streamed
     __threadfence();
     __syncthreads();
     for (int i = threadIdx.x; i < un.count; i += blockDim.x)
-        if (s_done[i] > 0) atomicAdd(f.ready + i, s_done[i]);
+        if (s_done[i] > 0) atomicAdd(f.ready + (long long)i * kReadyStride, s_done[i]);
     ffn_phase<NT, EPI_DOWN, true>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
 }
 

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     CTA_TRACE(p.trace);
     if (t == 0 && crank == 0 && threadIdx.x == 0 && p.stamp) *p.stamp = globaltimer();
     if (p.ffn_ready != nullptr && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < p.n_ready; i += blockDim.x) p.ffn_ready[i] = 0;
+        for (int i = threadIdx.x; i < p.n_ready; i += blockDim.x) p.ffn_ready[(long long)i * kReadyStride] = 0;
     phase_stamp(p.trace, 0);
     // ---- norm: thread owns groups of 8 consecutive columns (wide loads/stores)
     const float4* x4 = reinterpret_cast<const float4*>(p.x + (long long)t * p.d);
