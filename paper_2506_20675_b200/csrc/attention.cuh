@@ -140,6 +140,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
     griddep_wait();
     griddep_launch_early(kLateAttn);
     CTA_TRACE(p.trace);
+    phase_stamp(p.trace, 0);  // CTA 0 (diagnostic): 1 queries staged, 2 K/V ready, 3 partials stored
     prefetch_l2(p.pf, p.pf_bytes);
     const int n_items = nch * p.KV;
     const int QD = (p.H + 2 * p.KV) * HD;
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 }
             }
         }
+        if (item == (int)blockIdx.x) phase_stamp(p.trace, 1);
         if (has_new) {
             // the new keys of this chunk (positions ctx .. ctx+T-1, rotated)
             // and their values -> bf16, appended to the cache and staged at
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         kv_pending = false;
         cp_async_wait_all();
         __syncthreads();
+        if (item == (int)blockIdx.x) phase_stamp(p.trace, 2);
 
         for (int mt = warp; mt < n_mt; mt += kAttnThreads / 32) {
             const int r0 = mt * 16;
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
                 }
             }
         }
+        if (item == (int)blockIdx.x) phase_stamp(p.trace, 3);
         if (p.fused) {
             // arrival of this item; the last of the KV head's nch items
             // merges the head's chunk partials (fixed chunk order)

@@ -685,10 +685,12 @@ struct cascade_session {
     int pf_o = 0;          // attention CTAs (the whole grid) bulk-prefetch W_o into L2 after their wait
     int umma_no_trigger = 0;  // A/B: tcgen05 GEMVs let their dependents launch only at exit
     int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
+    int dense_pf = 0;      // tcgen05 GEMVs: rolling L2 prefetch this many ring stages ahead (CASCADE_DENSE_PF)
     int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
     int o_cluster = 0;     // same for the O projection
     int dn_prefetch = 8;   // fused FFN: k-steps of each warp's down range prefetched to L2 during the readiness wait (A/B: -1.5% at K=0)
     int min_seg = 8;       // k-steps per warp below which the stream-K split uses fewer pieces than CTAs
+    int par_topk = 1;      // router top-k by parallel rank counting (CASCADE_TOPK_PAR=0: k serial warp selections)
     uint16_t* kc = nullptr;
     uint16_t* vc = nullptr;
     float* logits_full = nullptr;  // taps only
@@ -902,6 +904,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_O")) s->pf_o = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = v[0] == '1';
+    if (const char* v = getenv("CASCADE_DENSE_PF")) s->dense_pf = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_UMMA_TRIGGER")) s->umma_no_trigger = v[0] == '0';
     if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = atoi(v);  // 1: whole range, n > 1: first n k-steps
     if (const char* v = getenv("CASCADE_GEMV_TRIGGER")) s->gemv_trigger = v[0] == '1';
@@ -912,6 +915,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
+    if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
     if (const char* v = getenv("CASCADE_DN_PF")) s->dn_prefetch = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
@@ -1082,6 +1086,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.no_prologue = !s->umma_prologue;
     p.ring_stages = s->cluster_stages;
     p.pf_self = s->pf_self;
+    p.pf_ahead = s->dense_pf;
     p.no_trigger = s->umma_no_trigger;
     return p;
 }
@@ -1325,6 +1330,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         rp.C = route_cluster(D, m->g.shared_gate);
         rp.ffn_ready = s->ffn_fused ? s->ffn_ready : nullptr;
         rp.n_ready = m->n_blocks;
+        rp.par_topk = s->par_topk;
         rp.stamp = s->stamps + 2 + 2 * l;
         rp.trace = tr(5);
         PB(5);

@@ -725,7 +725,10 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
                         __threadfence_block();
                     }
                     __syncwarp();
-                    if (!waited) cta_phase(p.trace, 3);  // first readiness wait of this warp released
+                    if (!waited) {
+                        cta_phase(p.trace, 3);  // first readiness wait of this warp released
+                        phase_stamp(p.trace, 5);
+                    }
                     waited = true;
                     ready_mask[bl >> 6] |= 1ull << (bl & 63);
                 }
@@ -778,6 +781,7 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
                 if (lane == 0) seg_unit[warp][slot] = unit;
             }
         }
+        if (item == wi) phase_stamp(p.trace, WAIT ? 6 : 1);  // CTA 0, warp 0: its range streamed
         __syncthreads();
 
         // ---- piece-level reduction of split super-tiles (owner = first contributor)
@@ -812,6 +816,7 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
             }
         }
         __syncthreads();  // red[] / seg_unit reused by the next item
+        if (item == wi) phase_stamp(p.trace, WAIT ? 7 : 2);  // CTA 0: piece-level reductions done
     }
     // ---- cross-piece reductions: every piece partial of this CTA is stored;
     //      one fence, then the arrivals; the last arriving piece of a
@@ -835,8 +840,9 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
         const int bl = (int)(unit / p.n_st);
         const int st = (int)(unit - (long long)bl * p.n_st);
         gemv_epilogue<NT, EPI>(p, bl, st, lane, acc, rk_row(bl));
-                if constexpr (!WAIT) { if (lane == 0) atomicAdd(s_done + bl, 1); }
+        if constexpr (!WAIT) { if (lane == 0) atomicAdd(s_done + bl, 1); }
     }
+    phase_stamp(p.trace, WAIT ? 8 : 3);  // CTA 0, warp 0: cross-CTA reductions done
 }
 
 struct FfnParams {
@@ -862,6 +868,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f
     CTA_TRACE(f.gu.trace);
     if (warp == 0) build_union(f.gu, un);
     __syncthreads();
+    phase_stamp(f.gu.trace, 0);  // CTA 0: union built (phases 1-3 gate/up, 4 published, 5-8 down)
     if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
     ffn_phase<NT, EPI_GATEUP, false>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
     cta_phase(f.gu.trace, 2);  // gate/up range of this CTA streamed
@@ -869,6 +876,7 @@ __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f
     __syncthreads();
     for (int i = threadIdx.x; i < un.count; i += blockDim.x)
         if (s_done[i] > 0) atomicAdd(f.ready + (long long)i * kReadyStride, s_done[i]);
+    phase_stamp(f.gu.trace, 4);
     ffn_phase<NT, EPI_DOWN, true>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
 }
 

@@ -119,6 +119,7 @@ struct UGemvParams {
     int ring_stages;           // dense_gemv_cluster_kernel: ring depth (<= kCMaxStages)
     int pf_self;               // dense_gemv_cluster_kernel: L2-prefetch the k-range beyond the ring before the wait
     int no_trigger;            // 1: dependents launch at exit, not right after the wait
+    int pf_ahead;              // rolling L2 prefetch: weights of the stage this many stages ahead of the ring
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -152,6 +153,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             su32(dst)),
         "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
         : "memory");
+}
+__device__ __forceinline__ void l2_prefetch_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -360,6 +364,15 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
                     unsigned char* dst = ring + (size_t)slot * kUStageBytes;
                     mb_expect_tx(&full_bar[slot], (uint32_t)n * (PROBE == 2 ? kUKsA : kUKsA + kUKsB));
                     bulk_g2s(dst, a, (uint32_t)n * kUKsA, &full_bar[slot], pol_a);
+                    if (with_b && p.pf_ahead > 0) {
+                        // rolling L2 prefetch: the piece's weights pf_ahead stages ahead
+                        // (flat (unit, k-step) positions are contiguous in the A layout)
+                        const long long f0 = p0 + (long long)p.pf_ahead * kUStageKs;
+                        if (f0 < hi) {
+                            const long long f1 = f0 + kUStageKs < hi ? f0 + kUStageKs : hi;
+                            l2_prefetch_bulk(p.W + (long long)blk * p.w_block_stride + f0 * (kUKsA / 2), (uint32_t)(f1 - f0) * kUKsA);
+                        }
+                    }
                     if (PROBE == 2) {
                     } else if (with_b) {
                         bulk_g2s(dst + kUStageA, p.B + b_off, (uint32_t)n * kUKsB, &full_bar[slot], pol_b);
@@ -383,6 +396,15 @@ __global__ void __launch_bounds__(kUThreads, 1) stream_gemv_umma_kernel(UGemvPar
             if (!early) {
                 U = p.count ? *p.count : p.n_blocks;
                 w = uwork(p, U);
+            }
+            if (p.pf_ahead > 0 && pos < hi) {
+                // fill the prefetch window once (the per-stage prefetch keeps it pf_ahead stages deep)
+                const int blk = p.list ? p.list[b] : b;
+                const long long f1 = pos + (long long)p.pf_ahead * kUStageKs < hi ? pos + (long long)p.pf_ahead * kUStageKs : hi;
+                for (long long f = pos; f < f1; f += kUStageKs) {
+                    const long long e = f + kUStageKs < f1 ? f + kUStageKs : f1;
+                    l2_prefetch_bulk(p.W + (long long)blk * p.w_block_stride + f * (kUKsA / 2), (uint32_t)(e - f) * kUKsA);
+                }
             }
             issue(0x7fffffff, true);
             udbg(p, 2);
@@ -631,11 +653,21 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         griddep_wait();
         if (!p.no_trigger) griddep_launch();
         if (lane == 0) {
+            // rolling L2 prefetch: the ring holds NS stages in flight per SM (the
+            // shared carveout caps it), so the weights of the next pf_ahead stages
+            // are requested into L2 ahead of their ring slot
+            auto pf_stage = [&](int j) {
+                if (j < n_stages)
+                    l2_prefetch_bulk(a_base + (long long)(ks_lo + j * kUStageKs) * (kUKsA / 2), (uint32_t)stage_n(j) * kUKsA);
+            };
+            const int i0 = p.no_prologue ? 0 : n_pre;
+            for (int j = i0; j < i0 + p.pf_ahead; ++j) pf_stage(j);
             for (int i = 0; i < n_stages; ++i) {
                 const int slot = i % NS;
                 const int n = stage_n(i);
                 const int ks = ks_lo + i * kUStageKs;
                 unsigned char* dst = ring + (size_t)slot * kUStageBytes;
+                if (i >= i0 && p.pf_ahead > 0) pf_stage(i + p.pf_ahead);
                 if (i >= n_pre || p.no_prologue) {
                     if (i >= NS) mb_wait(&empty_bar[slot], ((i / NS) - 1) & 1);
                     mb_expect_tx(&full_bar[slot], (uint32_t)n * (kUKsA + kUKsB));
@@ -674,9 +706,11 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         if (!p.no_trigger) griddep_launch();
         trace_start(p.trace);
         if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
+        phase_stamp(p.trace, 0);  // CTA 0 (diagnostic): 1 accumulator ready, 2 partials received, 3 epilogue done
         const int r = warp * 32 + lane;
         mb_wait(&acc_bar, 0);
         tc_fence_after();
+        phase_stamp(p.trace, 1);
         float val[16];
         tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16), val);
         tc_fence_before();
@@ -692,6 +726,7 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
             st_async_v4(raddr + q * 16, make_float4(val[4 * q], val[4 * q + 1], val[4 * q + 2], val[4 * q + 3]), rbar);
         if (r >= my_row0 && r < my_row0 + my_rows) {
             mb_wait(&recv_bar, 0);
+            phase_stamp(p.trace, 2);
             float acc[16];
 #pragma unroll
             for (int t = 0; t < 16; ++t) acc[t] = 0.f;
@@ -707,6 +742,7 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
                 }
             }
             uepilogue<EPI>(p, 0, unit, r, acc);
+            phase_stamp(p.trace, 3);
         }
     }
     tc_fence_before();

@@ -49,6 +49,7 @@ struct RouteParams {
     int C;                       // > 1: cluster of C CTAs per token, each staging 1/C of the router rows
     int* ffn_ready;              // fused expert FFN readiness counters: zeroed here, before this layer's FFN
     int n_ready;
+    int par_topk;                // 1: top-k by parallel rank counting (default); 0: k serial warp selections
     unsigned long long* stamp;   // MoE-block start (CostBreakdown split)
     unsigned long long* trace;
 };
@@ -288,6 +289,53 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_route_kernel(RouteParams p
     }
     __syncthreads();
     phase_stamp(p.trace, 2);
+    if (p.par_topk) {
+        // ---- top-k by rank: thread i counts the experts ordered before i
+        //      (larger logit first, lower index on ties); the k first ranks
+        //      are the selection in order.  The serial selection below costs
+        //      k rounds of 10 dependent shuffles (~2 us for OLMoE's k = 8).
+        __shared__ int s_sel[kMaxTopK];
+        if ((int)threadIdx.x < p.E) {
+            const int i = threadIdx.x;
+            const float vi = s_lg[i];
+            int rk = 0;
+#pragma unroll 8
+            for (int j = 0; j < p.E; ++j) {
+                const float vj = s_lg[j];
+                rk += (vj > vi || (vj == vi && j < i)) ? 1 : 0;
+            }
+            if (rk < p.k) s_sel[rk] = i;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            float m = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < kMaxExperts / 32; ++q) {
+                const int ei = lane + 32 * q;
+                m = fmaxf(m, ei < p.E ? s_lg[ei] : -INFINITY);
+            }
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            float z = 0.f;
+#pragma unroll
+            for (int q = 0; q < kMaxExperts / 32; ++q)
+                if (lane + 32 * q < p.E) z += __expf(s_lg[lane + 32 * q] - m);
+            for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+            float zk = 0.f, my_e = 0.f;
+            for (int r = 0; r < p.k; ++r) {  // same order as the serial selection: r = 0..k-1
+                const float ex = __expf(s_lg[s_sel[r]] - m);
+                zk += ex;
+                if (lane == r) my_e = ex;
+            }
+            const float den = p.renorm ? zk : z;
+            if (lane < p.k) {
+                p.topk_id[t * p.k + lane] = s_sel[lane];
+                p.topk_w[t * p.k + lane] = my_e / den;
+            }
+            if (lane == 0) p.gsh[t] = p.shared_gate ? 1.0f / (1.0f + __expf(-s_lg[p.E])) : 1.0f;
+        }
+        phase_stamp(p.trace, 3);
+        return;
+    }
     // ---- softmax + top-k of this token (warp 0)
     if (warp == 0) {
         const int tt = t;
