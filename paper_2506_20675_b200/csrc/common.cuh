@@ -119,6 +119,15 @@ __device__ __forceinline__ void phase_stamp(unsigned long long* slot, int i) {
     if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
     buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = globaltimer_raw();
 }
+// Per-warp stamp (diagnostic) of CTAs 0 and 1: stamp 16 + cta*16 + warp*2 + which
+// of the CTA-0 phase area (e.g. each warp's end of its gate/up and down ranges).
+__device__ __forceinline__ void warp_stamp(unsigned long long* slot, int which) {
+    unsigned long long* buf = g_cta_trace;
+    const int warp = threadIdx.x >> 5;
+    if (buf == nullptr || slot == nullptr || blockIdx.x > 1 || blockIdx.y != 0 || (threadIdx.x & 31) != 0 || warp > 7) return;
+    buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + 16 + blockIdx.x * 16 + warp * 2 + which] =
+        globaltimer_raw();
+}
 // Per-CTA phase stamp (diagnostic): record `which` (2 or 3) of this CTA
 // keeps the latest stamp of any warp that reports it.
 __device__ __forceinline__ void cta_phase(unsigned long long* slot, int which) {

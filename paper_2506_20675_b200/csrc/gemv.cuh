@@ -781,7 +781,10 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
                 if (lane == 0) seg_unit[warp][slot] = unit;
             }
         }
-        if (item == wi) phase_stamp(p.trace, WAIT ? 6 : 1);  // CTA 0, warp 0: its range streamed
+        if (item == wi) {
+            phase_stamp(p.trace, WAIT ? 6 : 1);  // CTA 0, warp 0: its range streamed
+            warp_stamp(p.trace, WAIT ? 1 : 0);   // CTAs 0-1, every warp (scripts/warp_spread.py)
+        }
         __syncthreads();
 
         // ---- piece-level reduction of split super-tiles (owner = first contributor)
