@@ -671,6 +671,7 @@ struct cascade_session {
     int attn_fused = 0;    // chunk combine inside the attention kernel (last item per KV head); A/B: the separate combine is as fast or faster
     int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
+    int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
     int* counters2 = nullptr;
@@ -914,6 +915,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_FUSED")) s->ffn_fused = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
+    if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
     if (const char* v = getenv("CASCADE_DN_PF")) s->dn_prefetch = std::max(0, atoi(v));
@@ -944,6 +946,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_smem_bytes<2>());
     if (e == cudaSuccess) e = carve(expert_ffn_kernel<1>);
     if (e == cudaSuccess) e = carve(expert_ffn_kernel<2>);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_smem_bytes<1>());
+    if (e == cudaSuccess) e = carve(expert_ffn_kernel<1, true>);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
@@ -1026,7 +1030,7 @@ static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaSt
 // launched cooperatively: the driver then guarantees co-residency (or fails
 // the launch with cudaErrorCooperativeLaunchTooLarge) even when other
 // sessions' kernels share the GPU, instead of relying on an idle device.
-static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop) {
+static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop, bool fma) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemvThreads);
@@ -1039,6 +1043,7 @@ static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, boo
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = coop ? 2 : 1;
+    if (fma && f.gu.T == 1) return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<1, true>, f);
     if (f.gu.T <= 8) return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<1>, f);
     return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<2>, f);
 }
@@ -1403,7 +1408,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             // its own loads 2x slower (A/B, profiles/r01f/ab_ffn_trigger.txt)
             fp.gu.trigger = s->ffn_trigger;
             PB(6);
-            CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop));
+            // CUDA-core single-token engine only outside batch-invariant mode (it
+            // would give the pending token other sums at K = 0 than at K > 0)
+            CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop, s->ffn_fma && !s->invariant));
             PE();
             ++nk;
         } else {

@@ -607,15 +607,52 @@ __global__ void __launch_bounds__(kGemvThreads, 2) stream_gemv_kernel(GemvParams
     }
 }
 
+// CUDA-core alternative for a single token (T = 1, K = 0 steps): the lane's
+// A-fragment holds rows g and g+8 at k = 2t..2t+1 and 2t+8..2t+9 of the
+// k-step; the token's activations at the same k come from lane t of the
+// B-fragment (token 0 lives in lanes 0-3).  Eight FMAs per tile, no tensor
+// core; the four partial sums of a row (the quad's lanes t = 0..3) are
+// added after the segment (fma_quad_to_acc), which leaves the mma.sync
+// accumulator layout so the reductions and epilogues are shared.
+__device__ __forceinline__ void fma_tile_t1(float (&pr)[2], const uint4& a, const uint2& b) {
+    const float x0 = __uint_as_float(b.x << 16), x1 = __uint_as_float(b.x & 0xFFFF0000u);
+    const float x8 = __uint_as_float(b.y << 16), x9 = __uint_as_float(b.y & 0xFFFF0000u);
+    float r0 = pr[0], r1 = pr[1];
+    r0 = fmaf(__uint_as_float(a.x << 16), x0, r0);
+    r0 = fmaf(__uint_as_float(a.x & 0xFFFF0000u), x1, r0);
+    r0 = fmaf(__uint_as_float(a.z << 16), x8, r0);
+    r0 = fmaf(__uint_as_float(a.z & 0xFFFF0000u), x9, r0);
+    r1 = fmaf(__uint_as_float(a.y << 16), x0, r1);
+    r1 = fmaf(__uint_as_float(a.y & 0xFFFF0000u), x1, r1);
+    r1 = fmaf(__uint_as_float(a.w << 16), x8, r1);
+    r1 = fmaf(__uint_as_float(a.w & 0xFFFF0000u), x9, r1);
+    pr[0] = r0;
+    pr[1] = r1;
+}
+template <int NT>
+__device__ __forceinline__ void fma_quad_to_acc(float (&pr)[kTPW][2], float (&acc)[kTPW][NT][4]) {
+#pragma unroll
+    for (int it = 0; it < kTPW; ++it)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float v = pr[it][h];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            acc[it][0][h * 2] = v;      // rows g / g+8, token 2t (token 0 on lanes t = 0)
+            acc[it][0][h * 2 + 1] = 0.f;
+        }
+}
+
 // One phase of the fused expert FFN (expert_ffn_kernel): the stream-K work
 // of stream_gemv_kernel for one matrix.  Phase 0 (gate/up) counts each
 // finished super-tile of slot bl in s_done[bl]; phase 1 (down) waits, per
 // slot, until ready[bl] reaches target (every gate/up super-tile of that
 // expert published) and reads its B operand (SiLU(gate)*up, written in this
 // launch) from L2.
-template <int NT, int EPI, bool WAIT>
+template <int NT, int EPI, bool WAIT, bool FMA = false>
 __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& un, int wi, int* s_done,
                                           const int* ready, int target) {
+    static_assert(!FMA || NT == 1, "the CUDA-core path serves one token");
     extern __shared__ float4 red[];
     __shared__ long long seg_unit[kGemvWarps][2];
     const bool routed = true;
@@ -734,8 +771,14 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
                 }
             }
             const uint4* A = p.W + (long long)blk * p.w_block_stride + (long long)st * p.n_ks * (kTPW * 32) + lane;
-            const uint2* Bp = p.B + (long long)bl * p.b_block_stride + lane;
+            // FMA: every lane reads token 0's B-fragment entry of its quad position (lane t)
+            const uint2* Bp = p.B + (long long)bl * p.b_block_stride + (FMA ? (lane & 3) : lane);
             zero_acc<NT>(acc);
+            float pr[kTPW][2];
+            if constexpr (FMA) {
+#pragma unroll
+                for (int it = 0; it < kTPW; ++it) pr[it][0] = pr[it][1] = 0.f;
+            }
             int s = ks0;
             for (; s + kUnroll <= ks1; s += kUnroll) {
                 uint2 bb[kUnroll][NT];
@@ -754,9 +797,13 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u)
 #pragma unroll
-                    for (int it = 0; it < kTPW; ++it)
+                    for (int it = 0; it < kTPW; ++it) {
+                        if constexpr (FMA) fma_tile_t1(pr[it], a[u][it], bb[u][0]);
+                        else {
 #pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], bb[u][nt]);
+                            for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a[u][it], bb[u][nt]);
+                        }
+                    }
             }
             for (; s < ks1; ++s) {
                 uint4 a1[kTPW];
@@ -766,10 +813,15 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) bb[nt] = WAIT ? ldcg_act(Bp + (s * 2 + nt) * 32) : ldg_act(Bp + (s * 2 + nt) * 32);
 #pragma unroll
-                for (int it = 0; it < kTPW; ++it)
+                for (int it = 0; it < kTPW; ++it) {
+                    if constexpr (FMA) fma_tile_t1(pr[it], a1[it], bb[0]);
+                    else {
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], bb[nt]);
+                        for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(acc[it][nt], a1[it], bb[nt]);
+                    }
+                }
             }
+            if constexpr (FMA) fma_quad_to_acc<NT>(pr, acc);
             const bool first_seg = pos == wlo;
             pos += ks1 - ks0;
             if (ks0 == 0 && ks1 == p.n_ks) {
@@ -860,7 +912,7 @@ struct FfnParams {
 // gate/up range, publishes the super-tiles it completed per expert (one
 // fence), and streams its down range; a down segment of expert b starts
 // once every gate/up super-tile of b is published.
-template <int NT>
+template <int NT, bool FMA = false>
 __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f) {
     __shared__ UnionSmem un;
     __shared__ int s_done[kMaxSlots];
@@ -873,14 +925,14 @@ __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f
     __syncthreads();
     phase_stamp(f.gu.trace, 0);  // CTA 0: union built (phases 1-3 gate/up, 4 published, 5-8 down)
     if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
-    ffn_phase<NT, EPI_GATEUP, false>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
+    ffn_phase<NT, EPI_GATEUP, false, FMA>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
     cta_phase(f.gu.trace, 2);  // gate/up range of this CTA streamed
     __threadfence();
     __syncthreads();
     for (int i = threadIdx.x; i < un.count; i += blockDim.x)
         if (s_done[i] > 0) atomicAdd(f.ready + (long long)i * kReadyStride, s_done[i]);
     phase_stamp(f.gu.trace, 4);
-    ffn_phase<NT, EPI_DOWN, true>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
+    ffn_phase<NT, EPI_DOWN, true, FMA>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
 }
 
 }  // namespace cascade
