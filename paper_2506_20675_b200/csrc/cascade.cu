@@ -671,6 +671,7 @@ struct cascade_session {
     int attn_fused = 0;    // chunk combine inside the attention kernel (last item per KV head); A/B: the separate combine is as fast or faster
     int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
+    int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
@@ -916,6 +917,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
+    if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
     if (const char* v = getenv("CASCADE_DN_PF")) s->dn_prefetch = std::max(0, atoi(v));
@@ -1103,6 +1105,7 @@ static GemvParams gemv_base(cascade_session* s, int T) {
     p.partial = s->partial;
     p.counters = s->counters;
     p.invariant = s->invariant;
+    p.unit_pieces = s->unit_pieces;
     p.sm_index = s->sm_index;
     p.sm_slot = s->sm_slot;
     p.cum = s->sm_cum;

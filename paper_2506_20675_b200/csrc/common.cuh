@@ -138,6 +138,17 @@ __device__ __forceinline__ void cta_phase(unsigned long long* slot, int which) {
     trace_start(slot);    \
     CtaExitStamp cta_exit_stamp_(slot)
 
+// gpu-scope release / acq_rel atomics (one lane publishes what its CTA
+// ordered before it with a barrier: PTX fences and release ops are cumulative)
+__device__ __forceinline__ void red_add_release(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atomic_add_acq_rel(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

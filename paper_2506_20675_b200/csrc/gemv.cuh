@@ -71,6 +71,7 @@ struct GemvParams {
     int publish;
     int* union_size;           // out (publish): distinct routed experts of the step
     int invariant;             // 1: fixed pieces per block (batch-invariant sums); 0: stream-K over all blocks
+    int unit_pieces;           // stream-K mode: one whole super-tile per CTA when the active super-tiles nearly fill the grid
     // SM-speed-weighted pieces: streaming rates differ by SM (a fixed
     // property of the part, +-3%; the slowest SM sets the kernel time), so
     // the work index of a CTA is (dense SM index, slot on that SM) and the
@@ -342,6 +343,15 @@ __device__ __forceinline__ void store_acc(float4* dst, const float (&acc)[kTPW][
 // speculative decoding bitwise lossless.  CTA c streams piece c of every
 // active block when P == grid (equal bytes per CTA for any U).
 __device__ __forceinline__ int block_pieces(const GemvParams& p, long long per_block) {
+    // Small experts (OLMoE at K = 0: 256 gate/up super-tiles of 256 KB for
+    // 296 CTAs): when the active super-tiles nearly fill the grid, one whole
+    // super-tile per CTA removes every cross-CTA partial (global partial
+    // store, fence, arrival atomic and reload) at the cost of idling the
+    // surplus CTAs; HBM stays saturated with >= 80% of the CTAs streaming.
+    if (p.unit_pieces && !p.invariant) {
+        const long long units = per_block / p.n_ks;
+        if (units <= (long long)gridDim.x && units * 5 >= (long long)gridDim.x * 4) return (int)units;
+    }
     long long pm = per_block / ((long long)p.min_seg * kGemvWarps);
     if (pm < 1) pm = 1;
     return pm < (long long)gridDim.x ? (int)pm : (int)gridDim.x;
@@ -876,7 +886,11 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
     // ---- cross-piece reductions: every piece partial of this CTA is stored;
     //      one fence, then the arrivals; the last arriving piece of a
     //      super-tile sums the piece partials in piece order
-    __threadfence();
+    // The barrier orders every warp's partial stores before the arrivals;
+    // each arrival is an acq_rel atomic by one lane (release: this CTA's
+    // partials; acquire: the other pieces' partials for the last arriver),
+    // instead of a gpu-scope fence by every thread (~1 us after a streaming
+    // phase, profiles/r02b).
     __syncthreads();
     const int np = n_pend < kMaxPend ? n_pend : kMaxPend;
     for (int e = warp; e < np; e += kGemvWarps) {
@@ -884,10 +898,10 @@ __device__ __forceinline__ void ffn_phase(const GemvParams& p, const UnionSmem& 
         const long long unit = pe.x;
         const int b = pe.y, first = pe.z, last = pe.w;
         int prev = 0;
-        if (lane == 0) prev = atomicAdd(p.counters + unit, 1);
+        if (lane == 0) prev = atomic_add_acq_rel(p.counters + unit, 1);
         prev = __shfl_sync(0xffffffffu, prev, 0);
         if (prev != last - first) continue;
-        __threadfence();
+        __syncwarp();
         zero_acc<NT>(acc);
         for (int j = first; j <= last; ++j)
             add_acc<NT>(acc, p.partial + (((long long)b * P + j) * 2 + (j == first ? 1 : 0)) * kSlot + lane, true);
@@ -927,10 +941,9 @@ __global__ void __launch_bounds__(kGemvThreads, 2) expert_ffn_kernel(FfnParams f
     if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
     ffn_phase<NT, EPI_GATEUP, false, FMA>(f.gu, un, (int)blockIdx.x, s_done, nullptr, 0);
     cta_phase(f.gu.trace, 2);  // gate/up range of this CTA streamed
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // every h store of the CTA is ordered before the release adds below
     for (int i = threadIdx.x; i < un.count; i += blockDim.x)
-        if (s_done[i] > 0) atomicAdd(f.ready + (long long)i * kReadyStride, s_done[i]);
+        if (s_done[i] > 0) red_add_release(f.ready + (long long)i * kReadyStride, s_done[i]);
     phase_stamp(f.gu.trace, 4);
     ffn_phase<NT, EPI_DOWN, true, FMA>(f.dn, un, (int)blockIdx.x, nullptr, f.ready, f.n_st_gu);
 }
