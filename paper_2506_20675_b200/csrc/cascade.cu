@@ -25,6 +25,7 @@
 #include "attention.cuh"
 #include "cascade.h"
 #include "common.cuh"
+#include "ffn_ring.cuh"
 #include "gemv.cuh"
 #include "init.cuh"
 #include "moe.cuh"
@@ -672,6 +673,7 @@ struct cascade_session {
     int ffn_trigger = 0;   // fused FFN: launch_dependents right after the wait (A/B: off is faster)
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
+    int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
@@ -917,6 +919,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
+    if (const char* v = getenv("CASCADE_FFN_RING")) s->ffn_ring = v[0] == '1';
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
@@ -950,6 +953,10 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = carve(expert_ffn_kernel<2>);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gemv_smem_bytes<1>());
     if (e == cudaSuccess) e = carve(expert_ffn_kernel<1, true>);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_ring_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, ffn_ring_smem_bytes<1>());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_ring_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ffn_ring_smem_bytes<2>());
+    if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<1>);
+    if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<2>);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
@@ -980,6 +987,15 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, expert_ffn_kernel<2>, kGemvThreads, gemv_smem_bytes<2>()) != cudaSuccess) {
             cudaGetLastError();
             o1 = o2 = 0;
+        }
+        if (s->ffn_ring) {
+            int r1 = 0, r2 = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, expert_ffn_ring_kernel<1>, kRingThreads, ffn_ring_smem_bytes<1>()) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, expert_ffn_ring_kernel<2>, kRingThreads, ffn_ring_smem_bytes<2>()) != cudaSuccess) {
+                cudaGetLastError();
+                r1 = r2 = 0;
+            }
+            if (std::min(r1, r2) < 1 || s->gemv_grid != 2 * m->num_sms) s->ffn_ring = 0;
         }
         if ((long long)std::min(o1, o2) * m->num_sms < s->gemv_grid) s->ffn_fused = 0;
     }
@@ -1032,11 +1048,12 @@ static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaSt
 // launched cooperatively: the driver then guarantees co-residency (or fails
 // the launch with cudaErrorCooperativeLaunchTooLarge) even when other
 // sessions' kernels share the GPU, instead of relying on an idle device.
-static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop, bool fma) {
+static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop, bool fma, bool ring) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kGemvThreads);
-    cfg.dynamicSmemBytes = f.gu.T <= 8 ? gemv_smem_bytes<1>() : gemv_smem_bytes<2>();
+    cfg.gridDim = dim3(ring ? grid / 2 : grid);  // ring: one CTA per SM
+    cfg.blockDim = dim3(ring ? kRingThreads : kGemvThreads);
+    cfg.dynamicSmemBytes = ring ? (f.gu.T <= 8 ? ffn_ring_smem_bytes<1>() : ffn_ring_smem_bytes<2>())
+                                : f.gu.T <= 8 ? gemv_smem_bytes<1>() : gemv_smem_bytes<2>();
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1045,6 +1062,8 @@ static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, boo
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = coop ? 2 : 1;
+    if (ring) return f.gu.T <= 8 ? cudaLaunchKernelEx(&cfg, expert_ffn_ring_kernel<1>, f)
+                                 : cudaLaunchKernelEx(&cfg, expert_ffn_ring_kernel<2>, f);
     if (fma && f.gu.T == 1) return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<1, true>, f);
     if (f.gu.T <= 8) return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<1>, f);
     return cudaLaunchKernelEx(&cfg, expert_ffn_kernel<2>, f);
@@ -1413,7 +1432,12 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             PB(6);
             // CUDA-core single-token engine only outside batch-invariant mode (it
             // would give the pending token other sums at K = 0 than at K > 0)
-            CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop, s->ffn_fma && !s->invariant));
+            // ring engine (one TMA stream per SM) for up to 8 tokens; with more
+            // the token block no longer fits L1 and the register engine is
+            // faster (A/B in profiles/r02b).  Batch-invariant mode keeps one
+            // engine for every T.
+            const bool ring = s->ffn_ring && !s->invariant && T <= 8;
+            CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop, s->ffn_fma && !s->invariant, ring));
             PE();
             ++nk;
         } else {
