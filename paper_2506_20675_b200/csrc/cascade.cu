@@ -674,6 +674,7 @@ struct cascade_session {
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
+    int ring_unit_pieces = 0;  // ring engine: allow one-super-tile pieces (CASCADE_RING_UNIT=1)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
@@ -920,6 +921,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_RING")) s->ffn_ring = v[0] == '1';
+    if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
@@ -1437,6 +1439,13 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             // faster (A/B in profiles/r02b).  Batch-invariant mode keeps one
             // engine for every T.
             const bool ring = s->ffn_ring && !s->invariant && T <= 8;
+            if (ring && !s->ring_unit_pieces) {
+                // one CTA per SM: whole super-tiles per CTA would idle SMs, and the
+                // ring finalises the two boundary super-tiles of a piece off the
+                // critical path anyway
+                fp.gu.unit_pieces = 0;
+                fp.dn.unit_pieces = 0;
+            }
             CK(launch_ffn(fp, s->gemv_grid, st, s->ffn_coop, s->ffn_fma && !s->invariant, ring));
             PE();
             ++nk;
