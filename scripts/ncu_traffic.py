@@ -31,12 +31,13 @@ def val(name):
 
 
 rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")
+kname = r[hdr.index("Kernel Name")].split("(")[0] if "Kernel Name" in hdr else "expert_ffn_kernel"
 us = [l for l in open(log) if l.startswith("union sizes")][-1]
 U0 = int(re.sub(r"np\.int\d+\((\d+)\)", r"\1", us.split(":", 1)[1]).strip(" []\n").split(",")[0])
 shape = cb.preset(config)
 alg = (U0 + shape.shared_experts) * 3 * shape.d_model * shape.d_ff * 2
 d = {"traffic_bytes_per_launch": rd + wr, "algorithmic_bytes_per_launch": alg,
-     "launch": f"expert_ffn_kernel (fused gate/up + SiLU + down), {config} layer 0, K={K}, U={U0} unique experts",
+     "launch": f"{kname} (fused gate/up + SiLU + down), {config} layer 0, K={K}, U={U0} unique experts",
      "source": os.path.basename(rep), "commit": commit, "command": command,
      "dram_read_bytes": rd, "dram_write_bytes": wr,
      "ratio_traffic_over_algorithmic": (rd + wr) / alg, "ratio_read_over_algorithmic": rd / alg,
