@@ -38,4 +38,11 @@ timeout 1200 ncu --set full --clock-control none --import-source on --profile-fr
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
   -k regex:"moe_route|moe_combine|attn_partial|attn_combine" -c 8 -o $O/small_full python scripts/profile_step.py --ks 0 --layers 2 > $O/prof_small.log 2>&1
 fi
+# summarise the full captures here and keep the reports off the copy-back (64 MiB cap)
+for r in gemv_full small_full ffn_traffic ffn_ring_traffic; do
+  [ -f $O/$r.ncu-rep ] && python scripts/ncu_summary.py $O/$r.ncu-rep $O/ncu_$r.csv > /dev/null 2>&1
+  [ -f $O/$r.ncu-rep ] && ncu -i $O/$r.ncu-rep --page details --csv > $O/ncu_${r}_details.csv 2>/dev/null
+  mkdir -p /tmp/ncu_reps && mv $O/$r.ncu-rep /tmp/ncu_reps/ 2>/dev/null
+done
+du -sh $O > $O/size.txt
 echo done > $O/DONE
