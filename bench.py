@@ -373,6 +373,17 @@ def run_ours(args, rank, world, local_rank):
             traffic_src = {k: pj.get(k) for k in ("launch", "source", "commit", "command")}
         except Exception:
             traffic = None
+    # the sweep runs the ring engine at K <= 7 and the register engine at K = 8:
+    # the ring engine's capture (K=4) is reported beside the K=8 one
+    ring_traffic = None
+    ring_path = os.path.join(ROOT, "profiles", "ncu_expert_ring_traffic.json")
+    if os.path.exists(ring_path):
+        try:
+            rj = json.load(open(ring_path))
+            ring_traffic = {k: rj.get(k) for k in ("traffic_bytes_per_launch", "algorithmic_bytes_per_launch",
+                                                   "ratio_traffic_over_algorithmic", "launch", "commit", "command")}
+        except Exception:
+            ring_traffic = None
     mean_bytes = float(np.mean([per_k[K]["bytes_gb"] for K in KS])) * 1e9
 
     # ---- e2e through the public call (host drafts in, host struct out, committing)
@@ -433,6 +444,7 @@ def run_ours(args, rank, world, local_rank):
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "traffic_algorithmic_bytes": traffic_alg,
                      "traffic_provenance": traffic_src,
+                     "traffic_ring_engine": ring_traffic,
                      "kernel": "expert GEMV (gate/up+SiLU and down), bytes = sum_l (U_l+S)*3*d*f*2",
                      "peak_kind": peak_kind,
                      "step_frac": round(mean_bytes / (value * 1e3) / peak, 4)},

@@ -119,6 +119,12 @@ __device__ __forceinline__ void phase_stamp(unsigned long long* slot, int i) {
     if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
     buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = globaltimer_raw();
 }
+// CTA-0 phase stamp from any single thread (phase_stamp is thread 0's)
+__device__ __forceinline__ void phase_stamp_cta0(unsigned long long* slot, int i) {
+    unsigned long long* buf = g_cta_trace;
+    if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0) return;
+    buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = globaltimer_raw();
+}
 // Per-warp stamp (diagnostic) of CTAs 0 and 1: stamp 16 + cta*16 + warp*2 + which
 // of the CTA-0 phase area (e.g. each warp's end of its gate/up and down ranges).
 __device__ __forceinline__ void warp_stamp(unsigned long long* slot, int which) {

@@ -219,6 +219,7 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
         };
         RingStage sg, sn;
         uint2 bb[kRingWarpKs][NT], bn[kRingWarpKs][NT];
+        bool first_stage = true;
         bool have = wk.next(p, sg);
         if (have) {
             if (down) ring_wait_ready(f, rs, sg.bl, ready_mask);
@@ -247,6 +248,10 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
             }
             __syncwarp();
             if (lane == 0) mb_arrive(&rs.empty[slot]);
+            if (first_stage) {
+                phase_stamp(f.gu.trace, down ? 4 : 1);  // CTA 0 warp 0: first stage of the phase consumed
+                first_stage = false;
+            }
             if (sg.ends) {
                 // hand this warp's partial of the super-tile to the finaliser
                 if (uc > 0) mb_wait(&rs.red_empty, (uc - 1) & 1);
@@ -256,7 +261,10 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
                 zero_acc<NT>(acc);
                 ++uc;
             }
-            if (!have_n) break;
+            if (!have_n) {
+                phase_stamp(f.gu.trace, down ? 5 : 2);  // CTA 0 warp 0: last stage of the phase consumed
+                break;
+            }
             sg = sn;
             if (pre) {
 #pragma unroll
@@ -326,6 +334,7 @@ __device__ __forceinline__ void ring_finalise(const FfnParams& f, const UnionSme
             }
         }
         if (phase == 0) cta_phase(f.gu.trace, 2);  // gate/up super-tiles of this CTA finalised
+        if (lane == 0) phase_stamp_cta0(f.gu.trace, phase ? 6 : 3);  // CTA 0 finaliser: phase finalised (0 union, 1-2 / 4-5 stream, 3 / 6 final)
     }
 }
 
