@@ -674,6 +674,7 @@ struct cascade_session {
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
+    int ring_dn_l2 = 0;    // ring engine: down stages L2-prefetched at the gate/up -> down transition (CASCADE_RING_DNPF)
     int ring_unit_pieces = 0;  // ring engine: allow one-super-tile pieces (CASCADE_RING_UNIT=1)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
@@ -922,6 +923,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_RING")) s->ffn_ring = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
+    if (const char* v = getenv("CASCADE_RING_DNPF")) s->ring_dn_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
@@ -1428,6 +1430,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             fp.dn.counters = s->counters2;
             fp.ready = s->ffn_ready;
             fp.n_st_gu = gu.n_st;
+            fp.dn_l2_stages = s->ring_dn_l2;
             // dependents launch at exit: an early-resident combine CTA made
             // its own loads 2x slower (A/B, profiles/r01f/ab_ffn_trigger.txt)
             fp.gu.trigger = s->ffn_trigger;

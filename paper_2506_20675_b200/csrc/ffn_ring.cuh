@@ -72,14 +72,21 @@ struct RingStage {
     bool ends;
 };
 
-// Walks this CTA's stages of one phase in order: item (block, piece), then
-// stages of <= kRingStageKs k-steps that never cross a super-tile.  The
-// position is advanced incrementally (64-bit divisions only once per item:
-// at 16 KB per stage they would cost more than the stage's MMAs).
+// Walks this CTA's stages of one phase: item (block, piece), then stages of
+// <= kRingStageKs k-steps that never cross a super-tile.  Inside a piece the
+// two super-tiles shared with the neighbouring pieces go first (the tail
+// part, then the head part, then the interior), so their cross-CTA partials
+// and arrivals are finished early, under the rest of the stream, and a
+// phase ends on an interior super-tile whose finalisation needs no global
+// round trip but the readiness publish.  The position advances
+// incrementally (64-bit divisions only at segment starts: per 32 KB stage
+// they would cost more than the stage's MMAs).
 struct RingWalk {
     RingGeo g;
     int n_ks, n_st, item, b, q;
-    long long base, clo, chi, pos;
+    long long base, clo, chi, pos, seg_end;
+    long long seg_lo[3], seg_hi[3];
+    int seg, n_seg;
     long long unit;
     int ks, bl, st;
     __device__ void start(const GemvParams& p, int U) {
@@ -87,33 +94,57 @@ struct RingWalk {
         n_ks = p.n_ks;
         n_st = p.n_st;
         item = (int)blockIdx.x - (int)gridDim.x;
-        pos = chi = 0;
+        pos = seg_end = 0;
+        seg = n_seg = 0;
+    }
+    __device__ void enter(long long at) {
+        pos = at;
+        unit = pos / n_ks;
+        ks = (int)(pos - unit * n_ks);
+        bl = (int)(unit / n_st);
+        st = (int)(unit - (long long)bl * n_st);
     }
     __device__ bool next(const GemvParams& p, RingStage& sg) {
-        while (pos >= chi) {
-            item += gridDim.x;
-            if (item >= g.n_items) return false;
-            b = item / g.P;
-            q = item - b * g.P;
-            base = (long long)b * g.per_block;
-            clo = base + piece_start(g.per_block, q, g.P, p.cum);
-            chi = base + piece_start(g.per_block, q + 1, g.P, p.cum);
-            pos = clo;
-            unit = pos / n_ks;
-            ks = (int)(pos - unit * n_ks);
-            bl = (int)(unit / n_st);
-            st = (int)(unit - (long long)bl * n_st);
+        while (pos >= seg_end) {
+            if (seg + 1 < n_seg) {
+                ++seg;
+            } else {
+                item += gridDim.x;
+                if (item >= g.n_items) return false;
+                b = item / g.P;
+                q = item - b * g.P;
+                base = (long long)b * g.per_block;
+                clo = base + piece_start(g.per_block, q, g.P, p.cum);
+                chi = base + piece_start(g.per_block, q + 1, g.P, p.cum);
+                if (chi <= clo) {
+                    n_seg = 0;
+                    continue;
+                }
+                const long long h1 = (clo / n_ks + 1) * n_ks;   // end of the head super-tile
+                const long long t0 = (chi - 1) / n_ks * n_ks;    // start of the tail super-tile
+                n_seg = 0;
+                if (h1 >= chi) {  // the piece lies in one super-tile
+                    seg_lo[n_seg] = clo, seg_hi[n_seg++] = chi;
+                } else {
+                    seg_lo[n_seg] = t0 > clo ? t0 : clo, seg_hi[n_seg++] = chi;     // tail part
+                    if (t0 > clo) seg_lo[n_seg] = clo, seg_hi[n_seg++] = h1;      // head part
+                    if (t0 > h1) seg_lo[n_seg] = h1, seg_hi[n_seg++] = t0;        // interior
+                }
+                seg = 0;
+            }
+            enter(seg_lo[seg]);
+            seg_end = seg_hi[seg];
         }
         const int rem_unit = n_ks - ks;
-        const long long rem_piece = chi - pos;
+        const long long rem_seg = seg_end - pos;
         int n = rem_unit < kRingStageKs ? rem_unit : kRingStageKs;
-        if (rem_piece < n) n = (int)rem_piece;
+        if (rem_seg < n) n = (int)rem_seg;
         sg.unit = unit;
         sg.ks = ks;
         sg.n = n;
         sg.bl = bl;
         sg.st = st;
-        sg.ends = n == rem_unit || n == rem_piece;
+        sg.ends = n == rem_unit || n == rem_seg;
         pos += n;
         ks += n;
         if (ks == n_ks) {
@@ -145,6 +176,21 @@ __device__ __forceinline__ void ring_producer(const FfnParams& f, const UnionSme
         RingWalk w;
         w.start(p, un.count);
         RingStage sg;
+        if (phase == 1 && f.dn_l2_stages > 0) {
+            // Down weights do not depend on gate/up, and HBM idles while the
+            // CTAs cross from gate/up to down (the last super-tiles' partials,
+            // the readiness publish and poll: ~10 us at Mixtral K=0/4): the
+            // down stages right behind the ring's first ones go to L2 now.
+            RingWalk pw;
+            pw.start(p, un.count);
+            RingStage ps;
+            int k = 0;
+            while (k < kRingStages + f.dn_l2_stages && pw.next(p, ps)) {
+                if (k++ < kRingStages) continue;
+                const uint4* src = p.W + (long long)un.list[ps.bl] * p.w_block_stride + ((long long)ps.st * p.n_ks + ps.ks) * (kTPW * 32);
+                l2_prefetch_bulk(src, (uint32_t)ps.n * kTPW * 32 * 16);
+            }
+        }
         while (w.next(p, sg)) {
             const int n = sg.n;
             const uint4* src = p.W + (long long)un.list[sg.bl] * p.w_block_stride + ((long long)sg.st * p.n_ks + sg.ks) * (kTPW * 32);
@@ -340,7 +386,7 @@ __device__ __forceinline__ void ring_finalise(const FfnParams& f, const UnionSme
 
 template <int NT>
 __global__ void __launch_bounds__(kRingThreads, 1) expert_ffn_ring_kernel(FfnParams f) {
-    extern __shared__ __align__(128) unsigned char ring[];
+    extern __shared__ __align__(1024) unsigned char ring[];
     float4* red = reinterpret_cast<float4*>(ring + (size_t)kRingStages * kRingStageBytes);
     __shared__ UnionSmem un;
     __shared__ RingSmem rs;

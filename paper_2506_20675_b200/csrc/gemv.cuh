@@ -918,6 +918,7 @@ struct FfnParams {
     GemvParams gu, dn;         // expert gate/up (EPI_GATEUP) and down (EPI_DOWN) launches' parameters
     int* ready;                // [slots] published gate/up super-tiles (zeroed by the combine kernel)
     int n_st_gu;               // gate/up super-tiles per expert
+    int dn_l2_stages;          // ring engine: down stages L2-prefetched at the gate/up -> down transition
 };
 
 // Fused expert FFN: gate/up (+SiLU) and down in one launch of 2 CTAs per SM
