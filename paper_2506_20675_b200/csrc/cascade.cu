@@ -674,6 +674,7 @@ struct cascade_session {
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
+    int ring_slot_major = 0;  // ring engine: per-slot pieces for large experts (CASCADE_RING_SLOTMAJOR=1)
     int ring_dn_l2 = 0;    // ring engine: down stages L2-prefetched at the gate/up -> down transition (CASCADE_RING_DNPF)
     int ring_unit_pieces = 0;  // ring engine: allow one-super-tile pieces (CASCADE_RING_UNIT=1)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
@@ -924,6 +925,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_RING")) s->ffn_ring = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_DNPF")) s->ring_dn_l2 = std::max(0, atoi(v));
+    if (const char* v = getenv("CASCADE_RING_SLOTMAJOR")) s->ring_slot_major = v[0] == '1';
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
@@ -1442,6 +1444,23 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             // faster (A/B in profiles/r02b).  Batch-invariant mode keeps one
             // engine for every T.
             const bool ring = s->ffn_ring && !s->invariant && T <= 8;
+            if (ring && s->ring_slot_major) {
+                // Slot-major pieces: every CTA streams its 1/grid of slot 0's
+                // gate/up, then of slot 1's, ..., then the same for down, so
+                // slot b's gate/up is complete chip-wide long before any CTA
+                // reaches slot b's down: no gate/up -> down readiness wait.
+                // Only for experts large enough that a slot's piece per CTA
+                // is >= min_seg k-steps per warp (P == grid for both phases).
+                auto pieces = [&](long long per_block) {
+                    long long pm = per_block / ((long long)s->min_seg * kGemvWarps);
+                    return pm < s->gemv_grid / 2 ? pm : (long long)(s->gemv_grid / 2);
+                };
+                const int g1 = s->gemv_grid / 2;
+                if (pieces((long long)gu.n_st * gu.n_ks) == g1 && pieces((long long)dn.n_st * dn.n_ks) == g1) {
+                    fp.gu.invariant = 1;
+                    fp.dn.invariant = 1;
+                }
+            }
             if (ring && !s->ring_unit_pieces) {
                 // one CTA per SM: whole super-tiles per CTA would idle SMs, and the
                 // ring finalises the two boundary super-tiles of a piece off the
