@@ -674,6 +674,7 @@ struct cascade_session {
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
+    int ring_max_t = 8;    // ring engine up to this many tokens (CASCADE_RING_MAXT; 16: every width)
     int ring_slot_major = 0;  // ring engine: per-slot pieces for large experts (CASCADE_RING_SLOTMAJOR=1)
     int ring_dn_l2 = 0;    // ring engine: down stages L2-prefetched at the gate/up -> down transition (CASCADE_RING_DNPF)
     int ring_unit_pieces = 0;  // ring engine: allow one-super-tile pieces (CASCADE_RING_UNIT=1)
@@ -926,6 +927,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_DNPF")) s->ring_dn_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_RING_SLOTMAJOR")) s->ring_slot_major = v[0] == '1';
+    if (const char* v = getenv("CASCADE_RING_MAXT")) s->ring_max_t = std::max(0, std::min(kMaxT, atoi(v)));
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
     if (const char* v = getenv("CASCADE_TOPK_PAR")) s->par_topk = v[0] == '1';
@@ -996,8 +998,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
         }
         if (s->ffn_ring) {
             int r1 = 0, r2 = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, expert_ffn_ring_kernel<1>, kRingThreads, ffn_ring_smem_bytes<1>()) != cudaSuccess ||
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, expert_ffn_ring_kernel<2>, kRingThreads, ffn_ring_smem_bytes<2>()) != cudaSuccess) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, expert_ffn_ring_kernel<1>, ffn_ring_threads<1>(), ffn_ring_smem_bytes<1>()) != cudaSuccess ||
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, expert_ffn_ring_kernel<2>, ffn_ring_threads<2>(), ffn_ring_smem_bytes<2>()) != cudaSuccess) {
                 cudaGetLastError();
                 r1 = r2 = 0;
             }
@@ -1057,7 +1059,7 @@ static cudaError_t launch_gemv_nt(int epi, const GemvParams& p, int grid, cudaSt
 static cudaError_t launch_ffn(const FfnParams& f, int grid, cudaStream_t st, bool coop, bool fma, bool ring) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ring ? grid / 2 : grid);  // ring: one CTA per SM
-    cfg.blockDim = dim3(ring ? kRingThreads : kGemvThreads);
+    cfg.blockDim = dim3(ring ? (f.gu.T <= 8 ? ffn_ring_threads<1>() : ffn_ring_threads<2>()) : kGemvThreads);
     cfg.dynamicSmemBytes = ring ? (f.gu.T <= 8 ? ffn_ring_smem_bytes<1>() : ffn_ring_smem_bytes<2>())
                                 : f.gu.T <= 8 ? gemv_smem_bytes<1>() : gemv_smem_bytes<2>();
     cfg.stream = st;
@@ -1443,7 +1445,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             // the token block no longer fits L1 and the register engine is
             // faster (A/B in profiles/r02b).  Batch-invariant mode keeps one
             // engine for every T.
-            const bool ring = s->ffn_ring && !s->invariant && T <= 8;
+            const bool ring = s->ffn_ring && !s->invariant && T <= s->ring_max_t;
             if (ring && s->ring_slot_major) {
                 // Slot-major pieces: every CTA streams its 1/grid of slot 0's
                 // gate/up, then of slot 1's, ..., then the same for down, so

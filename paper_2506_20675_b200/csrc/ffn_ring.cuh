@@ -35,18 +35,35 @@
 
 namespace cascade {
 
-constexpr int kRingStream = 4;                                 // stream (consumer) warps
-constexpr int kRingProducerWarp = kRingStream;                 // warp 4: TMA producer
-constexpr int kRingFinalWarp = kRingStream + 1;                // warp 5: finaliser
-constexpr int kRingThreads = 32 * (kRingStream + 2);
-constexpr int kRingWarpKs = 4;                                 // k-steps of a stage per stream warp
-constexpr int kRingStageKs = kRingWarpKs * kRingStream;        // 16 k-steps per stage
+constexpr int kRingStream = 4;                   // stream (consumer) warps 0-3
+constexpr int kRingProducerWarp = kRingStream;   // warp 4: weight (A) producer
+constexpr int kRingFinalWarp = kRingStream + 1;  // warp 5: finaliser
+constexpr int kRingBWarp = kRingStream + 2;      // warp 6 (T > 8 only): B-operand producer
 constexpr int kRingStages = 3;
-constexpr int kRingStageBytes = kRingStageKs * kTPW * 32 * 16;  // 32 KB
+constexpr int kBStepBytes = 2 * 32 * 8;          // B-frag bytes per k-step (both n8 token tiles)
+
+// Per token-tile geometry.  Up to 8 tokens (NT = 1) the token block fits
+// L1 and each stream warp loads its B-fragments itself (one stage of
+// look-ahead); with 9-16 tokens (NT = 2, up to 128 KB) it does not, and a
+// CTA sweeps the whole k-range once per super-tile, so every B load would
+// go to L2 under the weight stream: there the stage carries the B slice
+// too, copied by a second producer (which also owns the down phase's
+// readiness wait), and stages are 12 k-steps to fit the 132 KB carveout.
 template <int NT>
-constexpr int ffn_ring_smem_bytes() {
-    return kRingStages * kRingStageBytes + kRingStream * kTPW * NT * 32 * 16;
-}
+struct RingCfg {
+    static constexpr bool kBInStage = NT == 2;
+    static constexpr int kWarpKs = NT == 1 ? 4 : 3;                 // k-steps of a stage per stream warp
+    static constexpr int kStageKs = kWarpKs * kRingStream;            // 16 / 12
+    static constexpr int kABytes = kStageKs * kTPW * 32 * 16;         // 32 / 24 KB of weights
+    static constexpr int kStageBytes = kABytes + (kBInStage ? kStageKs * kBStepBytes : 0);
+    static constexpr int kThreads = 32 * (kRingStream + (kBInStage ? 3 : 2));
+    static constexpr int kSmem = kRingStages * kStageBytes + kRingStream * kTPW * NT * 32 * 16;
+};
+constexpr int kRingMaxThreads = RingCfg<2>::kThreads;
+template <int NT>
+constexpr int ffn_ring_smem_bytes() { return RingCfg<NT>::kSmem; }
+template <int NT>
+constexpr int ffn_ring_threads() { return RingCfg<NT>::kThreads; }
 
 // Geometry of one phase's split (the same pieces as ffn_phase: stream-K,
 // batch-invariant, or one super-tile per CTA).
@@ -73,7 +90,7 @@ struct RingStage {
 };
 
 // Walks this CTA's stages of one phase: item (block, piece), then stages of
-// <= kRingStageKs k-steps that never cross a super-tile.  Inside a piece the
+// <= sk k-steps that never cross a super-tile.  Inside a piece the
 // two super-tiles shared with the neighbouring pieces go first (the tail
 // part, then the head part, then the interior), so their cross-CTA partials
 // and arrivals are finished early, under the rest of the stream, and a
@@ -83,16 +100,17 @@ struct RingStage {
 // they would cost more than the stage's MMAs).
 struct RingWalk {
     RingGeo g;
-    int n_ks, n_st, item, b, q;
+    int n_ks, n_st, item, b, q, sk;
     long long base, clo, chi, pos, seg_end;
     long long seg_lo[3], seg_hi[3];
     int seg, n_seg;
     long long unit;
     int ks, bl, st;
-    __device__ void start(const GemvParams& p, int U) {
+    __device__ void start(const GemvParams& p, int U, int stage_ks) {
         g = ring_geo(p, U);
         n_ks = p.n_ks;
         n_st = p.n_st;
+        sk = stage_ks;
         item = (int)blockIdx.x - (int)gridDim.x;
         pos = seg_end = 0;
         seg = n_seg = 0;
@@ -137,7 +155,7 @@ struct RingWalk {
         }
         const int rem_unit = n_ks - ks;
         const long long rem_seg = seg_end - pos;
-        int n = rem_unit < kRingStageKs ? rem_unit : kRingStageKs;
+        int n = rem_unit < sk ? rem_unit : sk;
         if (rem_seg < n) n = (int)rem_seg;
         sg.unit = unit;
         sg.ks = ks;
@@ -162,11 +180,14 @@ struct RingWalk {
 struct RingSmem {
     uint64_t full[kRingStages], empty[kRingStages];
     uint64_t red_full, red_empty;
+    int a_issued;  // stages whose weight copy (and expect_tx) the A producer issued
     unsigned int ready_bits[(kMaxSlots + 31) / 32];
     int poll[kMaxSlots];
 };
 
+template <int NT>
 __device__ __forceinline__ void ring_producer(const FfnParams& f, const UnionSmem& un, unsigned char* ring, RingSmem& rs) {
+    using C = RingCfg<NT>;
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     int i = 0;
@@ -174,15 +195,14 @@ __device__ __forceinline__ void ring_producer(const FfnParams& f, const UnionSme
     for (int phase = 0; phase < 2; ++phase) {
         const GemvParams& p = phase ? f.dn : f.gu;
         RingWalk w;
-        w.start(p, un.count);
+        w.start(p, un.count, C::kStageKs);
         RingStage sg;
         if (phase == 1 && f.dn_l2_stages > 0) {
             // Down weights do not depend on gate/up, and HBM idles while the
-            // CTAs cross from gate/up to down (the last super-tiles' partials,
-            // the readiness publish and poll: ~10 us at Mixtral K=0/4): the
-            // down stages right behind the ring's first ones go to L2 now.
+            // CTAs cross from gate/up to down: optionally the down stages
+            // right behind the ring's first ones go to L2 now (A/B: no gain).
             RingWalk pw;
-            pw.start(p, un.count);
+            pw.start(p, un.count, C::kStageKs);
             RingStage ps;
             int k = 0;
             while (k < kRingStages + f.dn_l2_stages && pw.next(p, ps)) {
@@ -196,9 +216,60 @@ __device__ __forceinline__ void ring_producer(const FfnParams& f, const UnionSme
             const uint4* src = p.W + (long long)un.list[sg.bl] * p.w_block_stride + ((long long)sg.st * p.n_ks + sg.ks) * (kTPW * 32);
             const int slot = i % kRingStages;
             if (i >= kRingStages) mb_wait(&rs.empty[slot], ((i / kRingStages) - 1) & 1);
-            mb_expect_tx(&rs.full[slot], (uint32_t)n * kTPW * 32 * 16);
-            bulk_g2s(ring + (size_t)slot * kRingStageBytes, src, (uint32_t)n * kTPW * 32 * 16, &rs.full[slot], pol);
+            mb_expect_tx(&rs.full[slot], (uint32_t)n * (kTPW * 32 * 16 + (C::kBInStage ? kBStepBytes : 0)));
+            bulk_g2s(ring + (size_t)slot * C::kStageBytes, src, (uint32_t)n * kTPW * 32 * 16, &rs.full[slot], pol);
             ++i;
+            if constexpr (C::kBInStage) {
+                // the slot is free and its transaction count is set: the B
+                // producer may copy this stage's token slice
+                asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(su32(&rs.a_issued)), "r"(i) : "memory");
+            }
+        }
+    }
+}
+
+// B-operand producer (T > 8): copies each stage's token slice into the stage
+// right behind the weight copy; in the down phase it first waits for the
+// slot's readiness (every gate/up super-tile of that expert published), so
+// the stream warps never poll.
+template <int NT>
+__device__ __forceinline__ void ring_b_producer(const FfnParams& f, const UnionSmem& un, unsigned char* ring, RingSmem& rs) {
+    using C = RingCfg<NT>;
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    unsigned long long ready_mask[(kMaxSlots + 63) / 64] = {};
+    int i = 0;
+#pragma unroll 1
+    for (int phase = 0; phase < 2; ++phase) {
+        const GemvParams& p = phase ? f.dn : f.gu;
+        RingWalk w;
+        w.start(p, un.count, C::kStageKs);
+        RingStage sg;
+        while (w.next(p, sg)) {
+            const int bl = sg.bl;
+            if (phase == 1 && !((ready_mask[bl >> 6] >> (bl & 63)) & 1ull)) {
+                long long spins = 0;
+                for (;;) {
+                    int v;
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f.ready + (long long)bl * kReadyStride) : "memory");
+                    if (v >= f.n_st_gu) break;
+                    if (++spins > (1ll << 24)) __trap();  // a lost producer must not hang the GPU (~seconds)
+                    __nanosleep(32);
+                }
+                // the h stores of other CTAs (generic proxy) before this CTA's bulk copy of them
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                ready_mask[bl >> 6] |= 1ull << (bl & 63);
+            }
+            const int slot = i % kRingStages;
+            ++i;
+            for (;;) {
+                int v;
+                asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(su32(&rs.a_issued)) : "memory");
+                if (v >= i) break;
+                __nanosleep(20);
+            }
+            const uint2* src = p.B + (long long)bl * p.b_block_stride + (long long)sg.ks * (kBStepBytes / 8);
+            bulk_g2s(ring + (size_t)slot * C::kStageBytes + C::kABytes, src, (uint32_t)sg.n * kBStepBytes, &rs.full[slot], pol);
         }
     }
 }
@@ -233,10 +304,13 @@ __device__ __forceinline__ void ring_wait_ready(const FfnParams& f, RingSmem& rs
     ready_mask[bl >> 6] |= 1ull << (bl & 63);
 }
 
-// Stream warp w: k-steps 2w, 2w+1 of every stage of both phases.
+// Stream warp w: its k-steps of every stage of both phases (4w..4w+3 of 16
+// for NT = 1, 3w..3w+2 of 12 for NT = 2).
 template <int NT>
 __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem& un, const unsigned char* ring,
                                             float4* red, RingSmem& rs) {
+    using C = RingCfg<NT>;
+    constexpr int WK = C::kWarpKs;
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     constexpr int kSlot = kTPW * NT * 32;
@@ -249,39 +323,49 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
         const GemvParams& p = phase ? f.dn : f.gu;
         const bool down = phase == 1;
         RingWalk wk;
-        wk.start(p, un.count);
-        // one stage of look-ahead for the B-fragments: stage s+1's loads fly
-        // while stage s waits for its weights and runs its MMAs (a stage whose
-        // slot still needs its readiness wait loads after it)
-        const int k0 = kRingWarpKs * w;
-        auto load_b = [&](const RingStage& g, uint2 (&bb)[kRingWarpKs][NT]) {
+        wk.start(p, un.count, C::kStageKs);
+        const int k0 = WK * w;
+        // NT = 1: B-fragments from L1 with one stage of look-ahead (a stage
+        // whose slot still needs its readiness wait loads after it)
+        auto load_b = [&](const RingStage& g, uint2 (&bb)[WK][NT]) {
             const uint2* Bp = p.B + (long long)g.bl * p.b_block_stride + lane;
 #pragma unroll
-            for (int k = 0; k < kRingWarpKs; ++k)
+            for (int k = 0; k < WK; ++k)
                 if (k0 + k < g.n)
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
                         bb[k][nt] = down ? ldcg_act(Bp + ((g.ks + k0 + k) * 2 + nt) * 32) : ldg_act(Bp + ((g.ks + k0 + k) * 2 + nt) * 32);
         };
         RingStage sg, sn;
-        uint2 bb[kRingWarpKs][NT], bn[kRingWarpKs][NT];
-        bool first_stage = true;
+        uint2 bb[WK][NT], bn[WK][NT];
         bool have = wk.next(p, sg);
-        if (have) {
+        if (have && !C::kBInStage) {
             if (down) ring_wait_ready(f, rs, sg.bl, ready_mask);
             load_b(sg, bb);
         }
         while (have) {
             const bool have_n = wk.next(p, sn);
-            const bool pre = have_n && (!down || ((ready_mask[sn.bl >> 6] >> (sn.bl & 63)) & 1ull));
-            if (pre) load_b(sn, bn);
+            bool pre = false;
+            if constexpr (!C::kBInStage) {
+                pre = have_n && (!down || ((ready_mask[sn.bl >> 6] >> (sn.bl & 63)) & 1ull));
+                if (pre) load_b(sn, bn);
+            }
             const int n = sg.n;
             const int slot = i % kRingStages;
             mb_wait(&rs.full[slot], (i / kRingStages) & 1);
             ++i;
-            const uint4* S = reinterpret_cast<const uint4*>(ring + (size_t)slot * kRingStageBytes) + lane;
+            const unsigned char* stage = ring + (size_t)slot * C::kStageBytes;
+            if constexpr (C::kBInStage) {
+                const uint2* Bs = reinterpret_cast<const uint2*>(stage + C::kABytes) + lane;
 #pragma unroll
-            for (int k = 0; k < kRingWarpKs; ++k) {
+                for (int k = 0; k < WK; ++k)
+                    if (k0 + k < n)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) bb[k][nt] = Bs[((k0 + k) * 2 + nt) * 32];
+            }
+            const uint4* S = reinterpret_cast<const uint4*>(stage) + lane;
+#pragma unroll
+            for (int k = 0; k < WK; ++k) {
                 if (k0 + k < n) {
                     uint4 a[kTPW];
 #pragma unroll
@@ -294,10 +378,6 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
             }
             __syncwarp();
             if (lane == 0) mb_arrive(&rs.empty[slot]);
-            if (first_stage) {
-                phase_stamp(f.gu.trace, down ? 4 : 1);  // CTA 0 warp 0: first stage of the phase consumed
-                first_stage = false;
-            }
             if (sg.ends) {
                 // hand this warp's partial of the super-tile to the finaliser
                 if (uc > 0) mb_wait(&rs.red_empty, (uc - 1) & 1);
@@ -307,19 +387,18 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
                 zero_acc<NT>(acc);
                 ++uc;
             }
-            if (!have_n) {
-                phase_stamp(f.gu.trace, down ? 5 : 2);  // CTA 0 warp 0: last stage of the phase consumed
-                break;
-            }
+            if (!have_n) break;
             sg = sn;
-            if (pre) {
+            if constexpr (!C::kBInStage) {
+                if (pre) {
 #pragma unroll
-                for (int k = 0; k < kRingWarpKs; ++k)
+                    for (int k = 0; k < WK; ++k)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) bb[k][nt] = bn[k][nt];
-            } else {
-                ring_wait_ready(f, rs, sg.bl, ready_mask);
-                load_b(sg, bb);
+                        for (int nt = 0; nt < NT; ++nt) bb[k][nt] = bn[k][nt];
+                } else {
+                    ring_wait_ready(f, rs, sg.bl, ready_mask);
+                    load_b(sg, bb);
+                }
             }
         }
     }
@@ -338,7 +417,7 @@ __device__ __forceinline__ void ring_finalise(const FfnParams& f, const UnionSme
         const GemvParams& p = phase ? f.dn : f.gu;
         const bool down = phase == 1;
         RingWalk wk;
-        wk.start(p, un.count);
+        wk.start(p, un.count, RingCfg<NT>::kStageKs);
         RingStage sg;
         while (wk.next(p, sg)) {
             if (!sg.ends) continue;
@@ -385,9 +464,10 @@ __device__ __forceinline__ void ring_finalise(const FfnParams& f, const UnionSme
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kRingThreads, 1) expert_ffn_ring_kernel(FfnParams f) {
+__global__ void __launch_bounds__(kRingMaxThreads, 1) expert_ffn_ring_kernel(FfnParams f) {
+    using C = RingCfg<NT>;
     extern __shared__ __align__(1024) unsigned char ring[];
-    float4* red = reinterpret_cast<float4*>(ring + (size_t)kRingStages * kRingStageBytes);
+    float4* red = reinterpret_cast<float4*>(ring + (size_t)kRingStages * C::kStageBytes);
     __shared__ UnionSmem un;
     __shared__ RingSmem rs;
     const int warp = threadIdx.x >> 5;
@@ -398,6 +478,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) expert_ffn_ring_kernel(FfnPar
         }
         mb_init(&rs.red_full, kRingStream);
         mb_init(&rs.red_empty, 1);
+        rs.a_issued = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = threadIdx.x; i < (kMaxSlots + 31) / 32; i += blockDim.x) rs.ready_bits[i] = 0u;
@@ -410,9 +491,13 @@ __global__ void __launch_bounds__(kRingThreads, 1) expert_ffn_ring_kernel(FfnPar
     phase_stamp(f.gu.trace, 0);
     if (f.gu.publish && blockIdx.x == 0) publish_union(f.gu, un);
     if (warp == kRingProducerWarp) {
-        if ((threadIdx.x & 31) == 0) ring_producer(f, un, ring, rs);
+        if ((threadIdx.x & 31) == 0) ring_producer<NT>(f, un, ring, rs);
     } else if (warp == kRingFinalWarp) {
         ring_finalise<NT>(f, un, red, rs);
+    } else if (warp == kRingBWarp) {
+        if constexpr (C::kBInStage) {
+            if ((threadIdx.x & 31) == 0) ring_b_producer<NT>(f, un, ring, rs);
+        }
     } else {
         ring_stream<NT>(f, un, ring, red, rs);
     }
