@@ -146,7 +146,11 @@ def test_ring_and_register_ffn_engines_agree():
     (mr, ar, accr, ur, cr), (mg, ag, accg, ug, cg) = outs["ring"], outs["register"]
     assert cr == cg // 2, (cr, cg)  # one CTA per SM vs two
     assert ur == ug
-    rel = float(np.abs(mr - mg).max() / np.abs(mg).max())
-    print({"moe_rel_diff": rel, "ctas": (cr, cg)})
-    assert rel < 1e-4, rel
+    # layer 0 sees identical inputs: the engines differ only in fp32 summation
+    # order (and the rare bf16 rounding flip of an SiLU(gate)*up value it
+    # causes); layer 1's input already carries layer 0's difference
+    rel = [float(np.abs(mr[l] - mg[l]).max() / np.abs(mg[l]).max()) for l in range(2)]
+    print({"moe_rel_diff_per_layer": rel, "ctas": (cr, cg)})
+    assert rel[0] < 1e-3, rel
+    assert rel[1] < 1e-2, rel
     assert ar == ag and accr == accg
