@@ -338,6 +338,7 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
         };
         RingStage sg, sn;
         uint2 bb[WK][NT], bn[WK][NT];
+        bool first_stage = true;
         bool have = wk.next(p, sg);
         if (have && !C::kBInStage) {
             if (down) ring_wait_ready(f, rs, sg.bl, ready_mask);
@@ -378,6 +379,10 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
             }
             __syncwarp();
             if (lane == 0) mb_arrive(&rs.empty[slot]);
+            if (first_stage) {
+                phase_stamp(f.gu.trace, down ? 4 : 1);  // CTA 0 warp 0: first stage of the phase consumed
+                first_stage = false;
+            }
             if (sg.ends) {
                 // hand this warp's partial of the super-tile to the finaliser
                 if (uc > 0) mb_wait(&rs.red_empty, (uc - 1) & 1);
@@ -387,7 +392,10 @@ __device__ __forceinline__ void ring_stream(const FfnParams& f, const UnionSmem&
                 zero_acc<NT>(acc);
                 ++uc;
             }
-            if (!have_n) break;
+            if (!have_n) {
+                phase_stamp(f.gu.trace, down ? 5 : 2);  // CTA 0 warp 0: last stage of the phase consumed
+                break;
+            }
             sg = sn;
             if constexpr (!C::kBInStage) {
                 if (pre) {
