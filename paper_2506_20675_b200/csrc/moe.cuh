@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     float wk[8];  // the token's gate weights (rows 0..k-1 of its contribution list)
 #pragma unroll
     for (int q = 0; q < 8; ++q) wk[q] = q < p.k ? p.topk_w[t * p.k + q] : 0.f;
+    phase_stamp_after(p.trace, 4, wk[0] + g);  // diagnostic: gate weights arrived
     float4 nx[kG][2];
     float ss = 0.f;
 #pragma unroll
@@ -460,6 +461,7 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 if (q < nr) yb[q][h] = y4[(long long)q * n4 + 2 * c + h];
+        if (j == 0) phase_stamp_after(p.trace, 5, x0v[0].x + yb[0][0].x);  // diagnostic: residual + first contribution arrived
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = 2 * c + h;
