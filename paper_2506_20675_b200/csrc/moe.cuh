@@ -19,6 +19,7 @@
 
 #include <cooperative_groups.h>
 
+#include "combine_ops.cuh"
 #include "common.cuh"
 #include "gemv_umma.cuh"
 
@@ -54,11 +55,6 @@ struct RouteParams {
     unsigned long long* trace;
 };
 
-#ifndef CASCADE_ROW_THREADS
-#define CASCADE_ROW_THREADS 512
-#endif
-constexpr int kRowThreads = CASCADE_ROW_THREADS;  // route / combine: one CTA per token row
-constexpr int kRowG = 8192 / (8 * kRowThreads);   // 8-column groups per thread (d <= 8192)
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
 
@@ -75,11 +71,6 @@ __device__ __forceinline__ void store_b8(uint16_t* dst, bool umma, int t, int k0
         for (int q = 0; q < 4; ++q) *reinterpret_cast<uint32_t*>(dst + bfrag_index(t, k0 + 2 * q)) = w[q];
     }
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    return (uint32_t)bf16_bits(lo) | ((uint32_t)bf16_bits(hi) << 16);
-}
-__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // grid = T independent CTAs, CTA t = token t:
 //  * before griddepcontrol.wait (independent of the predecessor): the
@@ -470,18 +461,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
             for (int q = 0; q < kMaxR; ++q) {
                 if (q >= nr) break;
-                if (q < p.k) {
-                    const float w = wk[q];
-                    acc.x += w * yb[q][h].x;
-                    acc.y += w * yb[q][h].y;
-                    acc.z += w * yb[q][h].z;
-                    acc.w += w * yb[q][h].w;
-                } else {
-                    sh.x += yb[q][h].x;
-                    sh.y += yb[q][h].y;
-                    sh.z += yb[q][h].z;
-                    sh.w += yb[q][h].w;
-                }
+                if (q < p.k) moe_acc_add(acc, wk[q], yb[q][h]);
+                else moe_sh_add(sh, yb[q][h]);
             }
             for (int r0 = kMaxR; r0 < nr; r0 += 4) {  // rows beyond kMaxR: batches of 4, row order
                 float4 yr[4];
@@ -491,32 +472,17 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q;
-                    if (r < p.k) {
-                        const float w = p.topk_w[t * p.k + r];
-                        acc.x += w * yr[q].x;
-                        acc.y += w * yr[q].y;
-                        acc.z += w * yr[q].z;
-                        acc.w += w * yr[q].w;
-                    } else if (r < nr) {
-                        sh.x += yr[q].x;
-                        sh.y += yr[q].y;
-                        sh.z += yr[q].z;
-                        sh.w += yr[q].w;
-                    }
+                    if (r < p.k) moe_acc_add(acc, p.topk_w[t * p.k + r], yr[q]);
+                    else if (r < nr) moe_sh_add(sh, yr[q]);
                 }
             }
-            if (p.S > 0) {
-                acc.x += g * sh.x;
-                acc.y += g * sh.y;
-                acc.z += g * sh.z;
-                acc.w += g * sh.w;
-            }
-            if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
-            const float4 v = make_float4(x0.x + acc.x, x0.y + acc.y, x0.z + acc.z, x0.w + acc.w);
+            float4 moe;
+            const float4 v = moe_finish(x0, acc, sh, g, p.S > 0, moe);
+            if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = moe;
             nx[j][h] = v;
             x4[i] = v;
             if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = v;
-            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+            ss = ss_add(ss, v);
         }
     }
     phase_stamp(p.trace, 1);
@@ -527,12 +493,8 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     for (int j = 0; j < kG; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= n8) continue;
-        const float4 a = nx[j][0], b = nx[j][1];
-        uint32_t w[4];
-        w[0] = pack_bf16((a.x * rinv) * bf16_lo(nw[j].x), (a.y * rinv) * bf16_hi(nw[j].x));
-        w[1] = pack_bf16((a.z * rinv) * bf16_lo(nw[j].y), (a.w * rinv) * bf16_hi(nw[j].y));
-        w[2] = pack_bf16((b.x * rinv) * bf16_lo(nw[j].z), (b.y * rinv) * bf16_hi(nw[j].z));
-        w[3] = pack_bf16((b.z * rinv) * bf16_lo(nw[j].w), (b.w * rinv) * bf16_hi(nw[j].w));
+        const uint4 q = xn_pack8(nx[j][0], nx[j][1], rinv, nw[j]);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
         store_b8(p.xn_bfrag, p.umma != 0, t, 8 * c, w);
         if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
     }
