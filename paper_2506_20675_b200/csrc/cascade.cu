@@ -591,7 +591,7 @@ static cudaError_t launch_dense_cluster(int epi, const UGemvParams& p, int C, cu
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.n_st * C);
     cfg.blockDim = dim3(kUThreads);
-    cfg.dynamicSmemBytes = dense_cluster_smem_bytes(p.ring_stages) + (p.cmb_y ? dense_cluster_cmb_floats(p.cmb_d, C) * 4 : 0);
+    cfg.dynamicSmemBytes = dense_cluster_smem_bytes(p.ring_stages);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -638,7 +638,6 @@ struct cascade_session {
     cascade_verify_out* d_result = nullptr;
     cascade_verify_out* h_result = nullptr;
     float* x = nullptr;
-    float* x2 = nullptr;         // second residual buffer: a layer whose QKV folds the previous combine writes the other one
     uint16_t* xn = nullptr;      // MoE input (B-frag, expert GEMVs)
     uint16_t* xn_u = nullptr;    // attention / final-norm output (UMMA B layout for tcgen05 QKV / LM head)
     float* upartial = nullptr;   // tcgen05 engine split-unit partials
@@ -679,7 +678,6 @@ struct cascade_session {
     int ring_slot_major = 0;  // ring engine: per-slot pieces for large experts (CASCADE_RING_SLOTMAJOR=1)
     int ring_dn_l2 = 0;    // ring engine: down stages L2-prefetched at the gate/up -> down transition (CASCADE_RING_DNPF)
     int ring_unit_pieces = 0;  // ring engine: allow one-super-tile pieces (CASCADE_RING_UNIT=1)
-    int fuse_combine = 0;  // one-token steps: residual combine + RMSNorm folded into the next QKV GEMV (CASCADE_FUSE_COMBINE=1; A/B: slower)
     int ffn_fma = 0;       // fused FFN at T = 1 on CUDA-core FMAs instead of mma.sync (CASCADE_FFN_FMA=1; A/B: profiles/r02b)
     int ffn_coop = 1;      // cooperative launch of the fused FFN (co-residency guaranteed; CASCADE_FFN_COOP=0: plain launch)
     float4* partial2 = nullptr;  // the fused kernel's down-phase partials / counters
@@ -875,7 +873,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     };
     if ((rc = salloc(s, &s->d_params, sizeof(StepParams))) || (rc = salloc(s, &s->d_state, sizeof(DevState))) ||
         (rc = salloc(s, &s->d_result, sizeof(cascade_verify_out))) ||
-        (rc = salloc(s, &s->x, (size_t)kMaxT * D.d * 4)) || (rc = salloc(s, &s->x2, (size_t)kMaxT * D.d * 4)) || (rc = salloc(s, &s->xn, (size_t)D.d * 32)) ||
+        (rc = salloc(s, &s->x, (size_t)kMaxT * D.d * 4)) || (rc = salloc(s, &s->xn, (size_t)D.d * 32)) ||
         (rc = salloc(s, &s->xn_u, (size_t)D.d * 32)) ||
         (rc = salloc(s, &s->upartial, (size_t)m->num_sms * 2 * kUPartialFloats * 4, false)) ||
         (rc = salloc(s, &s->ucounters, (size_t)std::max({D.qkvd, D.d, D.V}) / kURows * 4)) ||
@@ -925,7 +923,6 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_FFN_TRIGGER")) s->ffn_trigger = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_COOP")) s->ffn_coop = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_FMA")) s->ffn_fma = v[0] == '1';
-    if (const char* v = getenv("CASCADE_FUSE_COMBINE")) s->fuse_combine = v[0] == '1';
     if (const char* v = getenv("CASCADE_FFN_RING")) s->ffn_ring = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_DNPF")) s->ring_dn_l2 = std::max(0, atoi(v));
@@ -968,7 +965,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_ring_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ffn_ring_smem_bytes<2>());
     if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<1>);
     if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<2>);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages) + dense_cluster_cmb_floats(D.d, 2) * 4);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (e == cudaSuccess) e = carve(dense_gemv_cluster_kernel<UEPI_STORE>);
@@ -1212,17 +1209,9 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
     ++nk;
 
     const int G = D.H / D.KV;
-    // One-token steps fold layer l's residual combine + layer l+1's RMSNorm
-    // into layer l+1's QKV GEMV (bitwise the combine kernel's result); the
-    // new residual then goes to the other buffer.
-    float* xres[2] = {s->x, s->x2};
-    int cur = 0;
-    const bool fuse = s->fuse_combine && T == 1 && m->umma_qkv() && s->qkv_cluster > 0 && m->comm == nullptr &&
-                      D.k + D.S <= 8 && D.d / 8 <= kRowThreads;
     for (int l = 0; l < D.L; ++l) {
         const LayerW& w = m->layers[l];
         const size_t td = (size_t)l * kMaxT * D.d;
-        const bool fused_in = fuse && l > 0;  // this QKV performs layer l-1's combine
         // QKV
         PB(1);
         if (m->umma_qkv()) {
@@ -1235,24 +1224,6 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             q.ld = D.qkvd;
             q.stamp = s->stamps + 1 + 2 * l;
             q.trace = tr(1);
-            if (fused_in) {
-                const size_t tp = (size_t)(l - 1) * kMaxT * D.d;  // layer l-1's taps (the combine's layer)
-                q.cmb_y = s->ycontrib;
-                q.cmb_x = xres[cur];
-                q.cmb_xout = xres[cur ^ 1];
-                q.cmb_w = s->topk_w;
-                q.cmb_g = s->gsh;
-                q.cmb_norm = w.attn_norm;
-                q.cmb_xn = s->xn_u;
-                q.cmb_k = D.k;
-                q.cmb_S = D.S;
-                q.cmb_d = D.d;
-                q.cmb_eps = m->g.norm_eps;
-                q.cmb_tap_moe = taps ? s->taps.moe_out + tp : nullptr;
-                q.cmb_tap_x = taps ? s->taps.x_in + td : nullptr;
-                q.cmb_tap_xn = taps ? s->taps.xn_attn + td : nullptr;
-                cur ^= 1;
-            }
             if (s->qkv_cluster) CK(launch_dense_cluster(UEPI_STORE, q, s->qkv_cluster, st));
             else CK(launch_ugemv(UEPI_STORE, q, m->num_sms, st));
         } else {
@@ -1346,7 +1317,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             o.B = s->attn_out;
             o.n_st = D.d / kURows;
             o.n_ks = D.hq / 16;
-            o.out = xres[cur];
+            o.out = s->x;
             o.ld = D.d;
             o.trace = tr(4);
             if (s->o_cluster) CK(launch_dense_cluster(UEPI_ADD, o, s->o_cluster, st));
@@ -1357,17 +1328,17 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             o.B = reinterpret_cast<const uint2*>(s->attn_out);
             o.n_st = D.d / kSTRows;
             o.n_ks = D.hq / 16;
-            o.out = xres[cur];
+            o.out = s->x;
             o.ld = D.d;
             o.trace = tr(4);
             CK(launch_gemv(EPI_ADD, o, s->gemv_grid, st));
         }
         PE();
         ++nk;
-        if (taps) CK(cudaMemcpyAsync(s->taps.x_mid + td, xres[cur], (size_t)T * D.d * 4, cudaMemcpyDeviceToDevice, st));
+        if (taps) CK(cudaMemcpyAsync(s->taps.x_mid + td, s->x, (size_t)T * D.d * 4, cudaMemcpyDeviceToDevice, st));
         // route: norm + router + top-k + union
         RouteParams rp{};
-        rp.x = xres[cur];
+        rp.x = s->x;
         rp.norm_w = w.ffn_norm;
         rp.router_w = w.router;
         rp.xn_bfrag = s->xn;
@@ -1520,9 +1491,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             PE();
             if (nr != 0) return set_err(CASCADE_ERUNTIME, "ncclAllReduce failed");
         }
-        if (fuse && l + 1 < D.L) continue;  // the next layer's QKV performs this combine
         CombineParams c{};
-        c.x = xres[cur];
+        c.x = s->x;
         c.ycontrib = s->ycontrib;
         c.topk_w = s->topk_w;
         c.gsh = s->gsh;

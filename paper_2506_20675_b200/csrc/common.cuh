@@ -119,15 +119,6 @@ __device__ __forceinline__ void phase_stamp(unsigned long long* slot, int i) {
     if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
     buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = globaltimer_raw();
 }
-// CTA-0 phase stamp that first waits for a loaded value (diagnostic: the
-// stamp measures the load's arrival, not its issue)
-__device__ __forceinline__ void phase_stamp_after(unsigned long long* slot, int i, float v) {
-    unsigned long long* buf = g_cta_trace;
-    if (buf == nullptr || slot == nullptr || blockIdx.x != 0 || blockIdx.y != 0 || threadIdx.x != 0) return;
-    unsigned long long t = globaltimer_raw();
-    if (v == -1.2345e-30f) t += 1;  // data dependence on v
-    buf[(slot - g_cta_trace_base) * kCtaTraceCap * kCtaRec + kPhaseBase * kCtaRec + i] = t;
-}
 // CTA-0 phase stamp from any single thread (phase_stamp is thread 0's)
 __device__ __forceinline__ void phase_stamp_cta0(unsigned long long* slot, int i) {
     unsigned long long* buf = g_cta_trace;

@@ -46,7 +46,6 @@
 // speculative decoding needs exactly that).
 #pragma once
 
-#include "combine_ops.cuh"
 #include "common.cuh"
 
 namespace cascade {
@@ -121,21 +120,6 @@ struct UGemvParams {
     int pf_self;               // dense_gemv_cluster_kernel: L2-prefetch the k-range beyond the ring before the wait
     int no_trigger;            // 1: dependents launch at exit, not right after the wait
     int pf_ahead;              // rolling L2 prefetch: weights of the stage this many stages ahead of the ring
-    // dense_gemv_cluster_kernel, one-token steps: the previous layer's residual
-    // combine + this layer's RMSNorm folded into the prologue (B = its output).
-    // cmb_y non-null: on.  Bitwise equal to moe_combine_kernel (combine_ops.cuh).
-    const float* cmb_y;        // ycontrib [1][k+S][d]
-    const float* cmb_x;        // residual in
-    float* cmb_xout;           // residual out (the other residual buffer; written by cluster 0)
-    const float* cmb_w;        // topk_w [1][k]
-    const float* cmb_g;        // shared-expert gate [1]
-    const uint16_t* cmb_norm;  // RMSNorm weights [d]
-    uint16_t* cmb_xn;          // B operand written here (UMMA B layout), then copied by TMA
-    int cmb_k, cmb_S, cmb_d;
-    float cmb_eps;
-    float* cmb_tap_moe;        // optional taps (cluster 0): MoE contribution, new residual, normed row
-    float* cmb_tap_x;
-    uint16_t* cmb_tap_xn;
 };
 
 // phase stamps for the probe: slot i <- globaltimer (CTA 0), or max/min over CTAs
@@ -571,9 +555,6 @@ constexpr int kCMaxStages = 6;
 constexpr int kCRecvFloats = (kURows + kCMaxC) * kUTok;  // sum over ranks of owned rows * 16
 
 constexpr int dense_cluster_smem_bytes(int stages) { return stages * kUStageBytes + kCRecvFloats * 4; }
-// + the fused combine's buffers: the CTA's columns of the new residual row,
-// the 512 per-thread partials of the row's sum of squares, 16 warp sums
-constexpr int dense_cluster_cmb_floats(int d, int C) { return (d / 16 / C + 2) * 16 + 512 + 16 + 4; }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -596,10 +577,6 @@ __device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t r
         "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
         : "memory");
 }
-__device__ __forceinline__ void st_async_f32(uint32_t raddr, float v, uint32_t rbar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr), "f"(v), "r"(rbar)
-                 : "memory");
-}
 __device__ __forceinline__ void cluster_sync_relaxed() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -616,8 +593,6 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
     __shared__ __align__(8) uint64_t empty_bar[kCMaxStages];
     __shared__ __align__(8) uint64_t acc_bar;
     __shared__ __align__(8) uint64_t recv_bar;
-    __shared__ __align__(8) uint64_t xn_bar;  // fused combine: B operand of this CTA's k-range stored
-    __shared__ __align__(8) uint64_t ssp_bar; // fused combine: the peers' sum-of-squares partials arrived
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -633,17 +608,8 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         }
         mb_init(&acc_bar, 1);
         mb_init(&recv_bar, 1);
-        mb_init(&xn_bar, 1);
-        mb_init(&ssp_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mb_expect_tx(&recv_bar, (uint32_t)(C * my_rows * kUTok * 4));
-        if (p.cmb_y != nullptr) {
-            // the 8-column groups (= combine threads) of the row with n8 <= 512:
-            // this CTA computes those of its k-range, the peers send theirs
-            const int n8 = p.cmb_d >> 3;
-            const int own = min(2 * ks_hi, n8) - min(2 * ks_lo, n8);
-            mb_expect_tx(&ssp_bar, (uint32_t)(n8 - own) * 4);
-        }
     }
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(&tmem_base_sh))
@@ -686,7 +652,6 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         }
         griddep_wait();
         if (!p.no_trigger) griddep_launch();
-        if (p.cmb_y != nullptr && lane == 0) mb_wait(&xn_bar, 0);  // the B operand is computed by this CTA first
         if (lane == 0) {
             // rolling L2 prefetch: the ring holds NS stages in flight per SM (the
             // shared carveout caps it), so the weights of the next pf_ahead stages
@@ -742,95 +707,6 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         trace_start(p.trace);
         if (p.stamp != nullptr && blockIdx.x == 0 && threadIdx.x == 0) *p.stamp = globaltimer();
         phase_stamp(p.trace, 0);  // CTA 0 (diagnostic): 1 accumulator ready, 2 partials received, 3 epilogue done
-        if (p.cmb_y != nullptr) {
-            // ---- previous layer's residual combine + this layer's RMSNorm for one
-            //      token, as moe_combine_kernel computes it: its thread vt owns the
-            //      8-column group vt (n8 <= 512), so each CTA of the cluster computes
-            //      the groups of its own k-range, sends their sum-of-squares partials
-            //      to the peers (st.async into their shared memory), and every CTA
-            //      runs the combine's reduction tree over all 512 partials; the
-            //      normed columns of the k-range become this CTA's B operand
-            float* vbuf = recv + kCRecvFloats;                           // this CTA's columns of the new residual
-            float* ssp = vbuf + (p.n_ks / C + 2) * 16;                   // [512] per-thread partials
-            float* red16 = ssp + 512;
-            const int tid = threadIdx.x;                                  // 0..127
-            const int d = p.cmb_d, n8 = d >> 3, n4 = d >> 2, nr = p.cmb_k + p.cmb_S;
-            const int col_lo = ks_lo * 16, col_hi = ks_hi * 16;
-            const int v_lo = min(2 * ks_lo, n8), v_hi = min(2 * ks_hi, n8);
-            const bool writer = unit == 0;                                // cluster 0 covers every column once
-            float wk[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) wk[q] = q < p.cmb_k ? p.cmb_w[q] : 0.f;
-            const float g = p.cmb_g[0];
-            const float4* y4 = reinterpret_cast<const float4*>(p.cmb_y);
-            const float4* x4 = reinterpret_cast<const float4*>(p.cmb_x);
-            for (int vt = n8 + tid; vt < 512; vt += 128) ssp[vt] = 0.f;  // combine threads without a group
-            const uint32_t lssp = su32(ssp);
-#pragma unroll 1
-            for (int vt0 = v_lo; vt0 < v_hi; vt0 += 256) {
-                // two groups per thread in flight together
-                float4 x0v[2][2], yb[2][8][2];
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int c = vt0 + tid + 128 * u;
-                    if (c >= v_hi) continue;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) x0v[u][h] = x4[2 * c + h];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-#pragma unroll
-                        for (int h = 0; h < 2; ++h)
-                            if (q < nr) yb[u][q][h] = y4[(long long)q * n4 + 2 * c + h];
-                }
-#pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int c = vt0 + tid + 128 * u;
-                    if (c >= v_hi) continue;
-                    float ss = 0.f;
-#pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), sh = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            if (q >= nr) break;
-                            if (q < p.cmb_k) moe_acc_add(acc, wk[q], yb[u][q][h]);
-                            else moe_sh_add(sh, yb[u][q][h]);
-                        }
-                        float4 moe;
-                        const float4 v = moe_finish(x0v[u][h], acc, sh, g, p.cmb_S > 0, moe);
-                        ss = ss_add(ss, v);
-                        *reinterpret_cast<float4*>(vbuf + (8 * c + 4 * h - col_lo)) = v;
-                        if (writer) {
-                            reinterpret_cast<float4*>(p.cmb_xout)[2 * c + h] = v;
-                            if (p.cmb_tap_moe) reinterpret_cast<float4*>(p.cmb_tap_moe)[2 * c + h] = moe;
-                            if (p.cmb_tap_x) reinterpret_cast<float4*>(p.cmb_tap_x)[2 * c + h] = v;
-                        }
-                    }
-                    ssp[c] = ss;
-                    for (int q = 0; q < C; ++q)
-                        if (q != rank) st_async_f32(mapa_shared(lssp + 4u * c, (uint32_t)q), ss, mapa_shared(su32(&ssp_bar), (uint32_t)q));
-                }
-            }
-            mb_wait(&ssp_bar, 0);
-            nbar(1, 128);
-            if (warp == 0) {
-                const float tot = block_sum512_emulated(ssp, red16);
-                if (lane == 0) red16[16] = tot;
-            }
-            nbar(1, 128);
-            const float rinv = 1.0f / sqrtf(red16[16] / (float)d + p.cmb_eps);
-            for (int c8 = col_lo / 8 + tid; c8 < col_hi / 8; c8 += 128) {
-                const float4 a = *reinterpret_cast<const float4*>(vbuf + 8 * c8 - col_lo);
-                const float4 b = *reinterpret_cast<const float4*>(vbuf + 8 * c8 - col_lo + 4);
-                const uint4 nw = __ldg(reinterpret_cast<const uint4*>(p.cmb_norm) + c8);
-                const uint4 q = xn_pack8(a, b, rinv, nw);
-                *reinterpret_cast<uint4*>(p.cmb_xn + umma_b_index(0, 8 * c8)) = q;
-                if (writer && p.cmb_tap_xn) *reinterpret_cast<uint4*>(p.cmb_tap_xn + 8 * c8) = q;
-            }
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> this CTA's bulk copies
-            nbar(1, 128);
-            if (tid == 0) mb_arrive(&xn_bar);
-        }
         const int r = warp * 32 + lane;
         mb_wait(&acc_bar, 0);
         tc_fence_after();

@@ -19,7 +19,6 @@
 
 #include <cooperative_groups.h>
 
-#include "combine_ops.cuh"
 #include "common.cuh"
 #include "gemv_umma.cuh"
 
@@ -55,6 +54,11 @@ struct RouteParams {
     unsigned long long* trace;
 };
 
+#ifndef CASCADE_ROW_THREADS
+#define CASCADE_ROW_THREADS 512
+#endif
+constexpr int kRowThreads = CASCADE_ROW_THREADS;  // route / combine: one CTA per token row
+constexpr int kRowG = 8192 / (8 * kRowThreads);   // 8-column groups per thread (d <= 8192)
 constexpr int kRowWarps = kRowThreads / 32;
 constexpr int kRouteStageBytes = 96 * 1024; // router weights staged in smem up to this size
 
@@ -71,6 +75,11 @@ __device__ __forceinline__ void store_b8(uint16_t* dst, bool umma, int t, int k0
         for (int q = 0; q < 4; ++q) *reinterpret_cast<uint32_t*>(dst + bfrag_index(t, k0 + 2 * q)) = w[q];
     }
 }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    return (uint32_t)bf16_bits(lo) | ((uint32_t)bf16_bits(hi) << 16);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // grid = T independent CTAs, CTA t = token t:
 //  * before griddepcontrol.wait (independent of the predecessor): the
@@ -434,7 +443,6 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     float wk[8];  // the token's gate weights (rows 0..k-1 of its contribution list)
 #pragma unroll
     for (int q = 0; q < 8; ++q) wk[q] = q < p.k ? p.topk_w[t * p.k + q] : 0.f;
-    phase_stamp_after(p.trace, 4, wk[0] + g);  // diagnostic: gate weights arrived
     float4 nx[kG][2];
     float ss = 0.f;
 #pragma unroll
@@ -452,7 +460,6 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 if (q < nr) yb[q][h] = y4[(long long)q * n4 + 2 * c + h];
-        if (j == 0) phase_stamp_after(p.trace, 5, x0v[0].x + yb[0][0].x);  // diagnostic: residual + first contribution arrived
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = 2 * c + h;
@@ -461,8 +468,18 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
             for (int q = 0; q < kMaxR; ++q) {
                 if (q >= nr) break;
-                if (q < p.k) moe_acc_add(acc, wk[q], yb[q][h]);
-                else moe_sh_add(sh, yb[q][h]);
+                if (q < p.k) {
+                    const float w = wk[q];
+                    acc.x += w * yb[q][h].x;
+                    acc.y += w * yb[q][h].y;
+                    acc.z += w * yb[q][h].z;
+                    acc.w += w * yb[q][h].w;
+                } else {
+                    sh.x += yb[q][h].x;
+                    sh.y += yb[q][h].y;
+                    sh.z += yb[q][h].z;
+                    sh.w += yb[q][h].w;
+                }
             }
             for (int r0 = kMaxR; r0 < nr; r0 += 4) {  // rows beyond kMaxR: batches of 4, row order
                 float4 yr[4];
@@ -472,17 +489,32 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int r = r0 + q;
-                    if (r < p.k) moe_acc_add(acc, p.topk_w[t * p.k + r], yr[q]);
-                    else if (r < nr) moe_sh_add(sh, yr[q]);
+                    if (r < p.k) {
+                        const float w = p.topk_w[t * p.k + r];
+                        acc.x += w * yr[q].x;
+                        acc.y += w * yr[q].y;
+                        acc.z += w * yr[q].z;
+                        acc.w += w * yr[q].w;
+                    } else if (r < nr) {
+                        sh.x += yr[q].x;
+                        sh.y += yr[q].y;
+                        sh.z += yr[q].z;
+                        sh.w += yr[q].w;
+                    }
                 }
             }
-            float4 moe;
-            const float4 v = moe_finish(x0, acc, sh, g, p.S > 0, moe);
-            if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = moe;
+            if (p.S > 0) {
+                acc.x += g * sh.x;
+                acc.y += g * sh.y;
+                acc.z += g * sh.z;
+                acc.w += g * sh.w;
+            }
+            if (p.tap_moe) reinterpret_cast<float4*>(p.tap_moe + (long long)t * p.d)[i] = acc;
+            const float4 v = make_float4(x0.x + acc.x, x0.y + acc.y, x0.z + acc.z, x0.w + acc.w);
             nx[j][h] = v;
             x4[i] = v;
             if (p.tap_x) reinterpret_cast<float4*>(p.tap_x + (long long)t * p.d)[i] = v;
-            ss = ss_add(ss, v);
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
         }
     }
     phase_stamp(p.trace, 1);
@@ -493,8 +525,12 @@ __global__ void __launch_bounds__(kRowThreads, 1) moe_combine_kernel(CombinePara
     for (int j = 0; j < kG; ++j) {
         const int c = threadIdx.x + j * kRowThreads;
         if (c >= n8) continue;
-        const uint4 q = xn_pack8(nx[j][0], nx[j][1], rinv, nw[j]);
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        const float4 a = nx[j][0], b = nx[j][1];
+        uint32_t w[4];
+        w[0] = pack_bf16((a.x * rinv) * bf16_lo(nw[j].x), (a.y * rinv) * bf16_hi(nw[j].x));
+        w[1] = pack_bf16((a.z * rinv) * bf16_lo(nw[j].y), (a.w * rinv) * bf16_hi(nw[j].y));
+        w[2] = pack_bf16((b.x * rinv) * bf16_lo(nw[j].z), (b.y * rinv) * bf16_hi(nw[j].z));
+        w[3] = pack_bf16((b.z * rinv) * bf16_lo(nw[j].w), (b.w * rinv) * bf16_hi(nw[j].w));
         store_b8(p.xn_bfrag, p.umma != 0, t, 8 * c, w);
         if (p.tap_xn) *reinterpret_cast<uint4*>(p.tap_xn + (long long)t * p.d + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
     }
