@@ -228,13 +228,27 @@ template <int EPI>
 __device__ __forceinline__ void uepilogue(const UGemvParams& p, int b, int st, int r, float (&v)[16]) {
     const int lane = threadIdx.x & 31;
     const long long row = (long long)st * kURows + r;
-    if constexpr (EPI == UEPI_STORE || EPI == UEPI_ADD) {
+    if constexpr (EPI == UEPI_ADD) {
+        // residual add: every token's old value is loaded before any store (a
+        // load-add-store per token in sequence could not be reordered by the
+        // compiler - the token rows might alias - and put T dependent L2
+        // round trips into the O projection's epilogue)
+        if (p.T == 1) {
+            p.out[row] += v[0];
+        } else {
+            float old[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t < p.T) old[t] = p.out[(long long)t * p.ld + row];
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (t < p.T) p.out[(long long)t * p.ld + row] = old[t] + v[t];
+        }
+    } else if constexpr (EPI == UEPI_STORE) {
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             if (t >= p.T) break;
-            float* o = p.out + (long long)t * p.ld + row;
-            if constexpr (EPI == UEPI_ADD) *o += v[t];
-            else *o = v[t];
+            p.out[(long long)t * p.ld + row] = v[t];
         }
     } else if constexpr (EPI == UEPI_GATEUP) {
         // 16-row groups: rows 0-7 gate j..j+7, rows 8-15 up j..j+7 (same warp)
