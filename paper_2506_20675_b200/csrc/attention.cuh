@@ -44,6 +44,7 @@ struct AttnParams {
     int* arrive;             // [KV] item arrivals (zero between launches)
     uint16_t* out_bfrag;     // [T][H*hd] bf16, UMMA B layout (umma) or B-frag
     int umma;
+    int ksplit;              // key-split chunk tiles (attn_ksplit_pass; hd >= 64)
 };
 
 // rotate_half RoPE on the pair (i, i + hd/2)
@@ -75,7 +76,7 @@ __device__ __forceinline__ void mma_bf16_regs(float (&c)[4], uint32_t a0, uint32
 
 template <int HD>
 constexpr int attn_smem_bytes(int qrows = kAttnMaxRows) {
-    return (2 * qrows + 2 * kChunk) * (HD + 8) * 2;
+    return (2 * qrows + 2 * kChunk) * (HD + 8) * 2 + 3 * (16 * (kChunk + 8) * 4 + 64 * 4);  // + key-split scratch (kAttnKsplitSmem)
 }
 
 // Two-term bf16 operands.  q and P enter the tensor cores as hi + lo bf16
@@ -93,6 +94,214 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Key-split chunk tiles (p.ksplit, hd >= 64).  The four warps share every
+// 16-row tile: warp w computes S for keys [16w, 16w+16) (32 mma instead of
+// 128), the chunk row max is exchanged through shared memory so every warp
+// exponentiates against the same max (P bitwise equal to the one-warp
+// tile), P is staged in fp32, and warp w then runs PV over all 64 keys
+// for dims [hd/4 * w, hd/4 * (w+1)) (32 mma instead of 128), splitting P
+// into its hi/lo bf16 terms as it loads the fragments.  Up to kAttnKsMt
+// row tiles go through one pass (two barriers per pass; the V fragments
+// are loaded once per pass).  Warp 0 forms the row sums from the staged P
+// in the one-warp tile's order, so the chunk partials (max, sum, o) are
+// bitwise those of the one-warp tile.
+constexpr int kAttnPLd = kChunk + 8;  // P row stride (fp32): conflict-free 8-byte fragment loads
+constexpr int kAttnKsMt = 3;          // row tiles per pass (4: register spills)
+constexpr int kAttnKsplitSmem = kAttnKsMt * (16 * kAttnPLd * 4 + 64 * 4);
+static_assert(attn_smem_bytes<128>(16) == (2 * 16 + 2 * kChunk) * 136 * 2 + kAttnKsplitSmem, "key-split scratch");
+
+template <int HD, int NM>
+__device__ __forceinline__ void attn_ksplit_pass(const AttnParams& p, const uint16_t* qs, const uint16_t* qsl,
+                                                 const uint16_t* ks, const uint16_t* vs, uint16_t* scratch,
+                                                 int mt0, int R, int nkeys, int key0, int ctx, int kvh, int c) {
+    constexpr int LD = HD + 8;
+    constexpr int NKS = HD / 16;
+    constexpr int NDW = HD / 32;  // n8 dim tiles per warp in PV
+    constexpr int MB = NM;  // row tiles of this pass
+    constexpr int PT = 16 * kAttnPLd;  // one P tile (fp32)
+    float* pe = reinterpret_cast<float*>(scratch);  // [kAttnKsMt][16][kAttnPLd] P (fp32)
+    float* red_m = pe + kAttnKsMt * PT;              // [kAttnKsMt][4 warps][16 rows]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    {
+        constexpr int nm = NM;
+        float s[MB][2][4];
+#pragma unroll
+        for (int u = 0; u < MB; ++u)
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s[u][nn][q] = 0.f;
+#pragma unroll
+        for (int kst = 0; kst < NKS; ++kst) {
+            const int i0 = kst * 16 + 2 * t4;
+            uint32_t b[2][2];
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) {
+                const int n = 2 * warp + nn;
+                b[nn][0] = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0);
+                b[nn][1] = *reinterpret_cast<const uint32_t*>(ks + (n * 8 + g) * LD + i0 + 8);
+            }
+#pragma unroll
+            for (int u = 0; u < MB; ++u) {
+                if (u >= nm) break;
+                const int r0 = (mt0 + u) * 16;
+                const uint32_t a0 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g) * LD + i0);
+                const uint32_t a1 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0);
+                const uint32_t a2 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g) * LD + i0 + 8);
+                const uint32_t a3 = *reinterpret_cast<const uint32_t*>(qs + (r0 + g + 8) * LD + i0 + 8);
+                const uint32_t l0 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g) * LD + i0);
+                const uint32_t l1 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g + 8) * LD + i0);
+                const uint32_t l2 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g) * LD + i0 + 8);
+                const uint32_t l3 = *reinterpret_cast<const uint32_t*>(qsl + (r0 + g + 8) * LD + i0 + 8);
+#pragma unroll
+                for (int nn = 0; nn < 2; ++nn) {
+                    mma_bf16_regs(s[u][nn], l0, l1, l2, l3, b[nn][0], b[nn][1]);
+                    mma_bf16_regs(s[u][nn], a0, a1, a2, a3, b[nn][0], b[nn][1]);
+                }
+            }
+        }
+        if (mt0 == 0) phase_stamp(p.trace, 4);  // CTA 0 (diagnostic): 4 S done, 5 max exchanged, 6 P staged, 7 PV done
+        // mask + this quarter's row max
+#pragma unroll
+        for (int u = 0; u < MB; ++u) {
+            if (u >= nm) break;
+            const int ra = (mt0 + u) * 16 + g, rb = ra + 8;
+            const int ta = ra % p.T, tb = rb % p.T;
+            float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int j = (2 * warp + nn) * 8 + 2 * t4 + (q & 1);
+                    const int tt = (q < 2) ? ta : tb;
+                    const bool ok = j < nkeys && key0 + j <= ctx + tt;  // causal on absolute positions
+                    if (!ok) s[u][nn][q] = -INFINITY;
+                    if (q < 2) ma = fmaxf(ma, s[u][nn][q]);
+                    else mb = fmaxf(mb, s[u][nn][q]);
+                }
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) {
+                ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+                mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+            }
+            if (t4 == 0) {
+                red_m[u * 64 + warp * 16 + g] = ma;
+                red_m[u * 64 + warp * 16 + g + 8] = mb;
+            }
+        }
+        __syncthreads();
+        if (mt0 == 0) phase_stamp(p.trace, 5);
+        // exponentiate against the chunk max, P -> smem
+#pragma unroll
+        for (int u = 0; u < MB; ++u) {
+            if (u >= nm) break;
+            const float* rm = red_m + u * 64;
+            const float ma = fmaxf(fmaxf(rm[g], rm[16 + g]), fmaxf(rm[32 + g], rm[48 + g]));
+            const float mb = fmaxf(fmaxf(rm[8 + g], rm[24 + g]), fmaxf(rm[40 + g], rm[56 + g]));
+            float* peu = pe + u * PT;
+#pragma unroll
+            for (int nn = 0; nn < 2; ++nn) {
+                float e[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float m = (q < 2) ? ma : mb;
+                    e[q] = (s[u][nn][q] == -INFINITY) ? 0.f : __expf(s[u][nn][q] - m);
+                }
+                const int col = (2 * warp + nn) * 8 + 2 * t4;
+                *reinterpret_cast<float2*>(peu + g * kAttnPLd + col) = make_float2(e[0], e[1]);
+                *reinterpret_cast<float2*>(peu + (g + 8) * kAttnPLd + col) = make_float2(e[2], e[3]);
+            }
+        }
+        __syncthreads();
+        if (mt0 == 0) phase_stamp(p.trace, 6);
+        // O = P V for this warp's dims, all row tiles of the pass
+        float o[MB][NDW][4];
+#pragma unroll
+        for (int u = 0; u < MB; ++u)
+#pragma unroll
+            for (int n = 0; n < NDW; ++n)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) o[u][n][q] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            uint32_t bv[NDW / 2][4];
+#pragma unroll
+            for (int n2 = 0; n2 < NDW / 2; ++n2) {
+                const int jrow = kk * 16 + (lane & 15);
+                const int col = (warp * NDW + 2 * n2) * 8 + ((lane >> 4) << 3);
+                const uint32_t addr = (uint32_t)__cvta_generic_to_shared(vs + jrow * LD + col);
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(bv[n2][0]), "=r"(bv[n2][1]), "=r"(bv[n2][2]), "=r"(bv[n2][3])
+                             : "r"(addr));
+            }
+            const int cA = kk * 16 + 2 * t4;
+#pragma unroll
+            for (int u = 0; u < MB; ++u) {
+                if (u >= nm) break;
+                const float* peu = pe + u * PT;
+                const float2 e0 = *reinterpret_cast<const float2*>(peu + g * kAttnPLd + cA);
+                const float2 e1 = *reinterpret_cast<const float2*>(peu + (g + 8) * kAttnPLd + cA);
+                const float2 e2 = *reinterpret_cast<const float2*>(peu + g * kAttnPLd + cA + 8);
+                const float2 e3 = *reinterpret_cast<const float2*>(peu + (g + 8) * kAttnPLd + cA + 8);
+                uint32_t a0, a1, a2, a3, l0, l1, l2, l3;
+                split_bf16x2(e0.x, e0.y, a0, l0);
+                split_bf16x2(e1.x, e1.y, a1, l1);
+                split_bf16x2(e2.x, e2.y, a2, l2);
+                split_bf16x2(e3.x, e3.y, a3, l3);
+#pragma unroll
+                for (int n2 = 0; n2 < NDW / 2; ++n2) {
+                    mma_bf16_regs(o[u][2 * n2], l0, l1, l2, l3, bv[n2][0], bv[n2][1]);
+                    mma_bf16_regs(o[u][2 * n2], a0, a1, a2, a3, bv[n2][0], bv[n2][1]);
+                    mma_bf16_regs(o[u][2 * n2 + 1], l0, l1, l2, l3, bv[n2][2], bv[n2][3]);
+                    mma_bf16_regs(o[u][2 * n2 + 1], a0, a1, a2, a3, bv[n2][2], bv[n2][3]);
+                }
+            }
+        }
+        if (mt0 == 0) phase_stamp(p.trace, 7);
+#pragma unroll
+        for (int u = 0; u < MB; ++u) {
+            if (u >= nm) break;
+            const float* rm = red_m + u * 64;
+            const int ra = (mt0 + u) * 16 + g, rb = ra + 8;
+            float la = 0.f, lb = 0.f;
+            if (warp == 0) {  // row sums in the one-warp tile's order: per lane over the 8 key tiles, then the quad
+                const float* peu = pe + u * PT;
+#pragma unroll
+                for (int n = 0; n < 8; ++n) {
+                    const float2 ea = *reinterpret_cast<const float2*>(peu + g * kAttnPLd + n * 8 + 2 * t4);
+                    const float2 eb = *reinterpret_cast<const float2*>(peu + (g + 8) * kAttnPLd + n * 8 + 2 * t4);
+                    la += ea.x;
+                    la += ea.y;
+                    lb += eb.x;
+                    lb += eb.y;
+                }
+#pragma unroll
+                for (int o = 1; o < 4; o <<= 1) {
+                    la += __shfl_xor_sync(0xffffffffu, la, o);
+                    lb += __shfl_xor_sync(0xffffffffu, lb, o);
+                }
+            }
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const int r = half ? rb : ra;
+                if (r >= R) continue;
+                float* out = p.part + (((long long)kvh * R + r) * p.max_chunks + c) * (HD + 2);
+#pragma unroll
+                for (int n = 0; n < NDW; ++n) {
+                    const int i = (warp * NDW + n) * 8 + 2 * t4;
+                    *reinterpret_cast<float2*>(out + 2 + i) = make_float2(o[u][n][half * 2 + 0], o[u][n][half * 2 + 1]);
+                }
+                if (warp == 0 && t4 == 0) {
+                    const int rr = g + 8 * half;
+                    out[0] = fmaxf(fmaxf(rm[rr], rm[16 + rr]), fmaxf(rm[32 + rr], rm[48 + rr]));
+                    out[1] = half ? lb : la;
+                }
+            }
+        }
+    }
+}
 
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
@@ -261,7 +470,23 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         __syncthreads();
         if (item == (int)blockIdx.x) phase_stamp(p.trace, 2);
 
-        for (int mt = warp; mt < n_mt; mt += kAttnThreads / 32) {
+        bool done_ksplit = false;
+        if constexpr (HD >= 64) {
+            if (p.ksplit) {
+                for (int mt0 = 0; mt0 < n_mt; mt0 += kAttnKsMt) {
+                    if (mt0 > 0) __syncthreads();  // the previous pass's readers of P / red_m are done
+                    uint16_t* scr = vs + kChunk * LD;
+                    switch (min(kAttnKsMt, n_mt - mt0)) {
+                        case 1: attn_ksplit_pass<HD, 1>(p, qs, qsl, ks, vs, scr, mt0, R, nkeys, key0, ctx, kvh, c); break;
+                        case 2: attn_ksplit_pass<HD, 2>(p, qs, qsl, ks, vs, scr, mt0, R, nkeys, key0, ctx, kvh, c); break;
+                        default: attn_ksplit_pass<HD, 3>(p, qs, qsl, ks, vs, scr, mt0, R, nkeys, key0, ctx, kvh, c); break;
+
+                    }
+                }
+                done_ksplit = true;
+            }
+        }
+        for (int mt = warp; mt < (done_ksplit ? 0 : n_mt); mt += kAttnThreads / 32) {
             const int r0 = mt * 16;
             // S = Q K^T  (16 rows x 64 keys)
             float s[8][4];
