@@ -303,6 +303,165 @@ __device__ __forceinline__ void attn_ksplit_pass(const AttnParams& p, const uint
     }
 }
 
+// Transposed key-split pass (p.ksplit == 2): S^T = K Q^T and O^T = V^T P^T
+// on mma.m16n8k16, so the query rows are the n8 dimension and a chunk item
+// with R rows costs ceil(R/8) row tiles instead of 2*ceil(R/16) (Mixtral
+// at K <= 1 and OLMoE / Qwen at K <= 7 have R <= 8: half the mma of the
+// key split above).  Warp w owns keys [16w, 16w+16) for S^T and dims
+// [hd/4 * w, hd/4 * (w+1)) for O^T; the row max is exchanged through
+// shared memory, P is staged in fp32 (split into hi/lo bf16 as the B
+// fragments load), and the row sums are formed in the one-warp tile's
+// order.  kAttnTRows rows per pass.
+constexpr int kAttnTRows = 32;
+static_assert(kAttnTRows * kAttnPLd * 4 + kAttnTRows * 4 * 4 <= kAttnKsplitSmem, "transposed pass scratch");
+
+template <int HD, int NB>
+__device__ __forceinline__ void attn_tpass(const AttnParams& p, const uint16_t* qs, const uint16_t* qsl,
+                                           const uint16_t* ks, const uint16_t* vs, uint16_t* scratch, int nr0,
+                                           int R, int nkeys, int key0, int ctx, int kvh, int c) {
+    constexpr int LD = HD + 8;
+    constexpr int NKS = HD / 16;
+    constexpr int MD = HD / 64;  // 16-dim m-tiles per warp in O^T
+    float* pe = reinterpret_cast<float*>(scratch);  // [kAttnTRows][kAttnPLd] P (fp32), by query row
+    float* red_m = pe + kAttnTRows * kAttnPLd;       // [kAttnTRows][4 warps]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int kw = warp * 16;
+    float s[NB][4];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[nb][q] = 0.f;
+#pragma unroll
+    for (int kst = 0; kst < NKS; ++kst) {
+        const int i0 = kst * 16 + 2 * t4;
+        const uint32_t a0 = *reinterpret_cast<const uint32_t*>(ks + (kw + g) * LD + i0);
+        const uint32_t a1 = *reinterpret_cast<const uint32_t*>(ks + (kw + g + 8) * LD + i0);
+        const uint32_t a2 = *reinterpret_cast<const uint32_t*>(ks + (kw + g) * LD + i0 + 8);
+        const uint32_t a3 = *reinterpret_cast<const uint32_t*>(ks + (kw + g + 8) * LD + i0 + 8);
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            const int row = (nr0 + nb) * 8 + g;
+            const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(qs + row * LD + i0);
+            const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(qs + row * LD + i0 + 8);
+            const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(qsl + row * LD + i0);
+            const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(qsl + row * LD + i0 + 8);
+            mma_bf16_regs(s[nb], a0, a1, a2, a3, bl0, bl1);
+            mma_bf16_regs(s[nb], a0, a1, a2, a3, bh0, bh1);
+        }
+    }
+    if (nr0 == 0) phase_stamp(p.trace, 4);
+    // mask; this key quarter's max of each row (lanes of equal t4 share rows)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        float m2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = (nr0 + nb) * 8 + 2 * t4 + h;
+            const int tt = r % p.T;
+#pragma unroll
+            for (int q = h; q < 4; q += 2) {
+                const int j = kw + g + (q >= 2 ? 8 : 0);
+                if (!(j < nkeys && key0 + j <= ctx + tt)) s[nb][q] = -INFINITY;
+            }
+            m2[h] = fmaxf(s[nb][h], s[nb][h + 2]);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) m2[h] = fmaxf(m2[h], __shfl_xor_sync(0xffffffffu, m2[h], o));
+        }
+        if (g == 0) {
+            red_m[(nb * 8 + 2 * t4) * 4 + warp] = m2[0];
+            red_m[(nb * 8 + 2 * t4 + 1) * 4 + warp] = m2[1];
+        }
+    }
+    __syncthreads();
+    if (nr0 == 0) phase_stamp(p.trace, 5);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int rl = nb * 8 + 2 * t4 + h;
+            const float m = fmaxf(fmaxf(red_m[rl * 4], red_m[rl * 4 + 1]), fmaxf(red_m[rl * 4 + 2], red_m[rl * 4 + 3]));
+#pragma unroll
+            for (int q = h; q < 4; q += 2) {
+                const float e = (s[nb][q] == -INFINITY) ? 0.f : __expf(s[nb][q] - m);
+                pe[rl * kAttnPLd + kw + g + (q >= 2 ? 8 : 0)] = e;
+            }
+        }
+    __syncthreads();
+    if (nr0 == 0) phase_stamp(p.trace, 6);
+    // O^T = V^T P^T for this warp's dims
+    float o[MD][NB][4];
+#pragma unroll
+    for (int md = 0; md < MD; ++md)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) o[md][nb][q] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        uint32_t av[MD][4];
+#pragma unroll
+        for (int md = 0; md < MD; ++md) {
+            const int d0 = (warp * MD + md) * 16;
+            const int key = kk * 16 + (lane & 7) + ((lane >> 4) << 3);
+            const int dim = d0 + (((lane >> 3) & 1) << 3);
+            const uint32_t addr = (uint32_t)__cvta_generic_to_shared(vs + key * LD + dim);
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(av[md][0]), "=r"(av[md][1]), "=r"(av[md][2]), "=r"(av[md][3])
+                         : "r"(addr));
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            const float* pr = pe + (nb * 8 + g) * kAttnPLd + kk * 16 + 2 * t4;
+            const float2 e0 = *reinterpret_cast<const float2*>(pr);
+            const float2 e1 = *reinterpret_cast<const float2*>(pr + 8);
+            uint32_t bh0, bl0, bh1, bl1;
+            split_bf16x2(e0.x, e0.y, bh0, bl0);
+            split_bf16x2(e1.x, e1.y, bh1, bl1);
+#pragma unroll
+            for (int md = 0; md < MD; ++md) {
+                mma_bf16_regs(o[md][nb], av[md][0], av[md][1], av[md][2], av[md][3], bl0, bl1);
+                mma_bf16_regs(o[md][nb], av[md][0], av[md][1], av[md][2], av[md][3], bh0, bh1);
+            }
+        }
+    }
+    if (nr0 == 0) phase_stamp(p.trace, 7);
+    // row max / sum (sum in the one-warp tile's order: per lane over the 8
+    // key tiles, then the quad)
+    for (int rl = threadIdx.x >> 2; rl < NB * 8; rl += kAttnThreads / 4) {
+        const float* pr = pe + rl * kAttnPLd + 2 * t4;
+        float l = 0.f;
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const float2 e = *reinterpret_cast<const float2*>(pr + n * 8);
+            l += e.x;
+            l += e.y;
+        }
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        const int r = nr0 * 8 + rl;
+        if (t4 == 0 && r < R) {
+            float* out = p.part + (((long long)kvh * R + r) * p.max_chunks + c) * (HD + 2);
+            out[0] = fmaxf(fmaxf(red_m[rl * 4], red_m[rl * 4 + 1]), fmaxf(red_m[rl * 4 + 2], red_m[rl * 4 + 3]));
+            out[1] = l;
+        }
+    }
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = (nr0 + nb) * 8 + 2 * t4 + h;
+            if (r >= R) continue;
+            float* out = p.part + (((long long)kvh * R + r) * p.max_chunks + c) * (HD + 2) + 2;
+#pragma unroll
+            for (int md = 0; md < MD; ++md) {
+                const int d0 = (warp * MD + md) * 16;
+                out[d0 + g] = o[md][nb][h];
+                out[d0 + g + 8] = o[md][nb][h + 2];
+            }
+        }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p) {
     constexpr int LD = HD + 8;
@@ -473,6 +632,19 @@ __global__ void __launch_bounds__(kAttnThreads) attn_partial_kernel(AttnParams p
         bool done_ksplit = false;
         if constexpr (HD >= 64) {
             if (p.ksplit) {
+                if (p.ksplit == 2) {
+                    const int NR = (R + 7) / 8;
+                    uint16_t* scr = vs + kChunk * LD;
+                    for (int nr0 = 0; nr0 < NR; nr0 += kAttnTRows / 8) {
+                        if (nr0 > 0) __syncthreads();  // the previous pass's readers of P / red_m are done
+                        switch (min(kAttnTRows / 8, NR - nr0)) {
+                            case 1: attn_tpass<HD, 1>(p, qs, qsl, ks, vs, scr, nr0, R, nkeys, key0, ctx, kvh, c); break;
+                            case 2: attn_tpass<HD, 2>(p, qs, qsl, ks, vs, scr, nr0, R, nkeys, key0, ctx, kvh, c); break;
+                            case 3: attn_tpass<HD, 3>(p, qs, qsl, ks, vs, scr, nr0, R, nkeys, key0, ctx, kvh, c); break;
+                            default: attn_tpass<HD, 4>(p, qs, qsl, ks, vs, scr, nr0, R, nkeys, key0, ctx, kvh, c); break;
+                        }
+                    }
+                } else
                 for (int mt0 = 0; mt0 < n_mt; mt0 += kAttnKsMt) {
                     if (mt0 > 0) __syncthreads();  // the previous pass's readers of P / red_m are done
                     uint16_t* scr = vs + kChunk * LD;

@@ -674,7 +674,10 @@ struct cascade_session {
     int ffn_fused = 1;     // expert gate/up + down in one launch (expert_ffn_kernel; CASCADE_FFN_FUSED=0: two launches)
     int unit_pieces = 1;   // expert GEMVs: whole super-tile per CTA when they nearly fill the grid (CASCADE_UNIT_PIECES=0: always stream-K)
     int ffn_ring = 1;      // fused FFN with one TMA stream per SM for T <= 8 (ffn_ring.cuh; CASCADE_FFN_RING=0: register engine)
-    int attn_ksplit = 1;   // key-split attention chunk tiles (CASCADE_ATTN_KSPLIT=0: one warp per 16-row tile)
+    // attention chunk tiles (CASCADE_ATTN_KSPLIT): 0 one warp per 16-row tile,
+    // 1 key split, 2 transposed key split, 3 per step width the one with
+    // fewer mma per warp (all four give bitwise-identical partials)
+    int attn_ksplit = 3;
     int ring_max_t = 8;    // ring engine up to this many tokens (CASCADE_RING_MAXT; 16: every width)
     int ring_slot_major = 0;  // ring engine: per-slot pieces for large experts (CASCADE_RING_SLOTMAJOR=1)
     int ring_dn_l2 = 0;    // ring engine: down stages L2-prefetched at the gate/up -> down transition (CASCADE_RING_DNPF)
@@ -928,7 +931,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_RING_UNIT")) s->ring_unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_RING_DNPF")) s->ring_dn_l2 = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_RING_SLOTMAJOR")) s->ring_slot_major = v[0] == '1';
-    if (const char* v = getenv("CASCADE_ATTN_KSPLIT")) s->attn_ksplit = atoi(v) != 0;
+    if (const char* v = getenv("CASCADE_ATTN_KSPLIT")) s->attn_ksplit = std::max(0, std::min(3, atoi(v)));
     if (const char* v = getenv("CASCADE_RING_MAXT")) s->ring_max_t = std::max(0, std::min(kMaxT, atoi(v)));
     if (const char* v = getenv("CASCADE_UNIT_PIECES")) s->unit_pieces = v[0] == '1';
     if (const char* v = getenv("CASCADE_MIN_SEG")) s->min_seg = std::max(1, atoi(v));
@@ -1286,7 +1289,12 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
         ap.arrive = s->attn_arrive;
         ap.out_bfrag = s->attn_out;
         ap.umma = m->umma_o();
-        ap.ksplit = s->attn_ksplit;
+        {
+            // mma per warp: key split 64 * ceil(R/16), transposed 32 * ceil(R/8)
+            // in passes of 4 row tiles -> transposed when ceil(R/8) is 1 or 3
+            const int nr = (G * T + 7) / 8;
+            ap.ksplit = s->attn_ksplit == 3 ? ((nr == 1 || nr == 3) ? 2 : 1) : s->attn_ksplit;
+        }
         PB(2);
         if (D.hd == 32) CK(launch_k(attn_partial_kernel<32>, agrid, kAttnThreads, asm_, st, true, ap));
         else if (D.hd == 64) CK(launch_k(attn_partial_kernel<64>, agrid, kAttnThreads, asm_, st, true, ap));
