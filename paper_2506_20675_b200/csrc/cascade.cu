@@ -563,12 +563,12 @@ __global__ void __launch_bounds__(kGemvThreads, 2) sm_rate_probe_kernel(const ui
 // Cluster size for the split-K dense GEMV over n_units 128-row units: the
 // largest C <= 8 with n_units * C <= SMs whose clusters can all be resident
 // at once (one wave); 0 = use the stream-K path.
-static int pick_cluster(const cascade_model* m, int n_units, int stages) {
+static int pick_cluster(const cascade_model* m, int n_units, int smem_bytes) {
     for (int C = std::min(kCMaxC, m->num_sms / std::max(n_units, 1)); C >= 2; --C) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(n_units * C);
         cfg.blockDim = dim3(kUThreads);
-        cfg.dynamicSmemBytes = dense_cluster_smem_bytes(stages);
+        cfg.dynamicSmemBytes = smem_bytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = C;
@@ -591,7 +591,7 @@ static cudaError_t launch_dense_cluster(int epi, const UGemvParams& p, int C, cu
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.n_st * C);
     cfg.blockDim = dim3(kUThreads);
-    cfg.dynamicSmemBytes = dense_cluster_smem_bytes(p.ring_stages);
+    cfg.dynamicSmemBytes = dense_cluster_smem_bytes(p.ring_stages, p.stage_ks);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -698,8 +698,10 @@ struct cascade_session {
     int umma_no_trigger = 0;  // A/B: tcgen05 GEMVs let their dependents launch only at exit
     int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
     int dense_pf = 0;      // tcgen05 GEMVs: rolling L2 prefetch this many ring stages ahead (CASCADE_DENSE_PF)
-    int cluster_stages = kUStages;  // ring depth of the split-K dense GEMV
+    int cluster_stages = kUStages;  // ring depth of the split-K O projection
     int o_cluster = 0;     // same for the O projection
+    int qkv_stages = 3;    // QKV ring: 3 stages of 16 k-steps (64 KB of weights each; A/B in DESIGN §4)
+    int qkv_stage_ks = kCMaxStageKs;
     int dn_prefetch = 8;   // fused FFN: k-steps of each warp's down range prefetched to L2 during the readiness wait (A/B: -1.5% at K=0)
     int min_seg = 8;       // k-steps per warp below which the stream-K split uses fewer pieces than CTAs
     int par_topk = 1;      // router top-k by parallel rank counting (CASCADE_TOPK_PAR=0: k serial warp selections)
@@ -939,6 +941,12 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (const char* v = getenv("CASCADE_DN_PF")) s->dn_prefetch = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_INVARIANT")) s->invariant = v[0] == '1';
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
+    if (const char* v = getenv("CASCADE_QKV_STAGE_KS")) s->qkv_stage_ks = std::max(1, std::min(kCMaxStageKs, atoi(v)));
+    if (const char* v = getenv("CASCADE_QKV_STAGES")) s->qkv_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
+    if (dense_cluster_smem_bytes(s->qkv_stages, s->qkv_stage_ks) > 227 * 1024) {  // an override that does not fit
+        s->qkv_stages = kUStages;
+        s->qkv_stage_ks = kUStageKs;
+    }
     if (const char* v = getenv("CASCADE_LATE_TRIGGER")) {
         const int late = (v[0] == '1' && v[1] == 0) ? 31 : atoi(v);  // "1": every latency-bound kernel; else a kLate* mask
         cudaMemcpyToSymbol(g_late_trigger, &late, sizeof(late));
@@ -970,7 +978,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) e = cudaFuncSetAttribute(expert_ffn_ring_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, ffn_ring_smem_bytes<2>());
     if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<1>);
     if (e == cudaSuccess) e = carve(expert_ffn_ring_kernel<2>);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   std::max(dense_cluster_smem_bytes(s->cluster_stages), dense_cluster_smem_bytes(s->qkv_stages, s->qkv_stage_ks)));
     if (e == cudaSuccess) e = cudaFuncSetAttribute(dense_gemv_cluster_kernel<UEPI_ADD>, cudaFuncAttributeMaxDynamicSharedMemorySize, dense_cluster_smem_bytes(s->cluster_stages));
     if (const char* v = getenv("CASCADE_CLUSTER_STAGES")) s->cluster_stages = std::max(2, std::min(kCMaxStages, atoi(v)));
     if (e == cudaSuccess) e = carve(dense_gemv_cluster_kernel<UEPI_STORE>);
@@ -978,8 +987,8 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     if (e == cudaSuccess) {
         bool on = true;
         if (const char* v = getenv("CASCADE_DENSE_CLUSTER")) on = v[0] == '1';
-        if (on && m->umma_qkv()) s->qkv_cluster = pick_cluster(m, D.qkvd / kURows, s->cluster_stages);
-        if (on && m->umma_o()) s->o_cluster = pick_cluster(m, D.d / kURows, s->cluster_stages);
+        if (on && m->umma_qkv()) s->qkv_cluster = pick_cluster(m, D.qkvd / kURows, dense_cluster_smem_bytes(s->qkv_stages, s->qkv_stage_ks));
+        if (on && m->umma_o()) s->o_cluster = pick_cluster(m, D.d / kURows, dense_cluster_smem_bytes(s->cluster_stages));
     }
     if (e != cudaSuccess) {
         set_err(CASCADE_ECUDA, cudaGetErrorString(e));
@@ -1124,6 +1133,7 @@ static UGemvParams ugemv_base(cascade_session* s, int T) {
     p.counters = s->ucounters;
     p.no_prologue = !s->umma_prologue;
     p.ring_stages = s->cluster_stages;
+    p.stage_ks = kUStageKs;
     p.pf_self = s->pf_self;
     p.pf_ahead = s->dense_pf;
     p.no_trigger = s->umma_no_trigger;
@@ -1229,6 +1239,8 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             q.ld = D.qkvd;
             q.stamp = s->stamps + 1 + 2 * l;
             q.trace = tr(1);
+            q.ring_stages = s->qkv_stages;
+            q.stage_ks = s->qkv_stage_ks;
             if (s->qkv_cluster) CK(launch_dense_cluster(UEPI_STORE, q, s->qkv_cluster, st));
             else CK(launch_ugemv(UEPI_STORE, q, m->num_sms, st));
         } else {

@@ -117,6 +117,7 @@ struct UGemvParams {
     unsigned long long* dbg;   // optional phase stamps (scripts/umma_probe.cu)
     int no_prologue;           // A/B: issue nothing before griddepcontrol.wait
     int ring_stages;           // dense_gemv_cluster_kernel: ring depth (<= kCMaxStages)
+    int stage_ks;              // dense_gemv_cluster_kernel: k-steps per ring stage (<= kCMaxStageKs)
     int pf_self;               // dense_gemv_cluster_kernel: L2-prefetch the k-range beyond the ring before the wait
     int no_trigger;            // 1: dependents launch at exit, not right after the wait
     int pf_ahead;              // rolling L2 prefetch: weights of the stage this many stages ahead of the ring
@@ -568,7 +569,16 @@ constexpr int kCMaxC = 8;
 constexpr int kCMaxStages = 6;
 constexpr int kCRecvFloats = (kURows + kCMaxC) * kUTok;  // sum over ranks of owned rows * 16
 
-constexpr int dense_cluster_smem_bytes(int stages) { return stages * kUStageBytes + kCRecvFloats * 4; }
+// Ring stages of the split-K engine are sized at launch: QKV, whose
+// predecessor (the one-CTA residual combine) leaves the SMs free, streams
+// 3 x 64 KB stages (225 KB of shared memory); the O projection keeps
+// 3 x 32 KB so that its CTAs fit beside the attention CTAs they follow and
+// prefetch their weights under them (PDL prologue).
+constexpr int kCMaxStageKs = 16;
+__host__ __device__ constexpr int dense_cluster_stage_bytes(int stage_ks) { return stage_ks * (kUKsA + kUKsB); }
+constexpr int dense_cluster_smem_bytes(int stages, int stage_ks = kUStageKs) {
+    return stages * dense_cluster_stage_bytes(stage_ks) + kCRecvFloats * 4;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -602,7 +612,9 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
     static_assert(EPI == UEPI_STORE || EPI == UEPI_ADD, "cluster split-K: row-local epilogues only");
     extern __shared__ __align__(1024) unsigned char ring[];
     const int NS = p.ring_stages;
-    float* recv = reinterpret_cast<float*>(ring + (size_t)NS * kUStageBytes);  // [src][own row][16]
+    const int SK = p.stage_ks;                          // k-steps per stage
+    const int SB = dense_cluster_stage_bytes(SK), SA = SK * kUKsA;
+    float* recv = reinterpret_cast<float*>(ring + (size_t)NS * SB);  // [src][own row][16]
     __shared__ __align__(8) uint64_t full_bar[kCMaxStages];
     __shared__ __align__(8) uint64_t empty_bar[kCMaxStages];
     __shared__ __align__(8) uint64_t acc_bar;
@@ -643,21 +655,21 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_a));
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_b));
         const uint16_t* a_base = p.W + ((long long)unit * p.n_ks) * (kUKsA / 2);
-        const int n_stages = (ks_hi - ks_lo + kUStageKs - 1) / kUStageKs;
-        auto stage_n = [&](int i) { return min(kUStageKs, ks_hi - (ks_lo + i * kUStageKs)); };
+        const int n_stages = (ks_hi - ks_lo + SK - 1) / SK;
+        auto stage_n = [&](int i) { return min(SK, ks_hi - (ks_lo + i * SK)); };
         // PDL prologue: the weights do not depend on the predecessor
         const int n_pre = min(NS, n_stages);
         if (lane == 0 && !p.no_prologue) {
             for (int i = 0; i < n_pre; ++i) {
                 const int n = stage_n(i);
                 mb_expect_tx(&full_bar[i], (uint32_t)n * (kUKsA + kUKsB));
-                bulk_g2s(ring + (size_t)i * kUStageBytes, a_base + (long long)(ks_lo + i * kUStageKs) * (kUKsA / 2),
+                bulk_g2s(ring + (size_t)i * SB, a_base + (long long)(ks_lo + i * SK) * (kUKsA / 2),
                          (uint32_t)n * kUKsA, &full_bar[i], pol_a);
             }
             if (p.pf_self) {
                 // the rest of this CTA's weights -> L2 while the latency-bound predecessor runs
-                const char* src = reinterpret_cast<const char*>(a_base + (long long)(ks_lo + n_pre * kUStageKs) * (kUKsA / 2));
-                const long long bytes = (long long)(ks_hi - (ks_lo + n_pre * kUStageKs)) * kUKsA;
+                const char* src = reinterpret_cast<const char*>(a_base + (long long)(ks_lo + n_pre * SK) * (kUKsA / 2));
+                const long long bytes = (long long)(ks_hi - (ks_lo + n_pre * SK)) * kUKsA;
                 for (long long off = 0; off < bytes; off += 32768) {
                     const uint32_t sz = (uint32_t)(bytes - off < 32768 ? bytes - off : 32768);
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + off), "r"(sz) : "memory");
@@ -672,22 +684,22 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
             // are requested into L2 ahead of their ring slot
             auto pf_stage = [&](int j) {
                 if (j < n_stages)
-                    l2_prefetch_bulk(a_base + (long long)(ks_lo + j * kUStageKs) * (kUKsA / 2), (uint32_t)stage_n(j) * kUKsA);
+                    l2_prefetch_bulk(a_base + (long long)(ks_lo + j * SK) * (kUKsA / 2), (uint32_t)stage_n(j) * kUKsA);
             };
             const int i0 = p.no_prologue ? 0 : n_pre;
             for (int j = i0; j < i0 + p.pf_ahead; ++j) pf_stage(j);
             for (int i = 0; i < n_stages; ++i) {
                 const int slot = i % NS;
                 const int n = stage_n(i);
-                const int ks = ks_lo + i * kUStageKs;
-                unsigned char* dst = ring + (size_t)slot * kUStageBytes;
+                const int ks = ks_lo + i * SK;
+                unsigned char* dst = ring + (size_t)slot * SB;
                 if (i >= i0 && p.pf_ahead > 0) pf_stage(i + p.pf_ahead);
                 if (i >= n_pre || p.no_prologue) {
                     if (i >= NS) mb_wait(&empty_bar[slot], ((i / NS) - 1) & 1);
                     mb_expect_tx(&full_bar[slot], (uint32_t)n * (kUKsA + kUKsB));
                     bulk_g2s(dst, a_base + (long long)ks * (kUKsA / 2), (uint32_t)n * kUKsA, &full_bar[slot], pol_a);
                 }
-                bulk_g2s(dst + kUStageA, p.B + (long long)ks * (kUKsB / 2), (uint32_t)n * kUKsB, &full_bar[slot], pol_b);
+                bulk_g2s(dst + SA, p.B + (long long)ks * (kUKsB / 2), (uint32_t)n * kUKsB, &full_bar[slot], pol_b);
             }
         }
     } else if (warp == 5) {
@@ -695,17 +707,17 @@ __global__ void __launch_bounds__(kUThreads, 1) dense_gemv_cluster_kernel(UGemvP
         griddep_wait();
         if (!p.no_trigger) griddep_launch();
         if (lane == 0) {
-            const int n_stages = (ks_hi - ks_lo + kUStageKs - 1) / kUStageKs;
+            const int n_stages = (ks_hi - ks_lo + SK - 1) / SK;
             bool first = true;
             for (int i = 0; i < n_stages; ++i) {
                 const int slot = i % NS;
-                const int n = min(kUStageKs, ks_hi - (ks_lo + i * kUStageKs));
+                const int n = min(SK, ks_hi - (ks_lo + i * SK));
                 mb_wait(&full_bar[slot], (i / NS) & 1);
                 tc_fence_after();
-                const unsigned char* st = ring + (size_t)slot * kUStageBytes;
+                const unsigned char* st = ring + (size_t)slot * SB;
                 for (int j = 0; j < n; ++j) {
                     const uint64_t da = umma_desc(st + j * kUKsA, 2048, 128);
-                    const uint64_t db = umma_desc(st + kUStageA + j * kUKsB, 256, 128);
+                    const uint64_t db = umma_desc(st + SA + j * kUKsB, 256, 128);
                     umma_bf16(tmem, da, db, first ? 0u : 1u);
                     first = false;
                 }
