@@ -201,3 +201,46 @@ def test_key_split_attention_is_bitwise_the_one_warp_tile(name, arm):
         assert np.array_equal(xa.view(np.uint32), xb.view(np.uint32)), float(np.abs(xa - xb).max())
         assert np.array_equal(la.view(np.uint32), lb.view(np.uint32)), float(np.abs(la - lb).max())
         assert aa == ab
+
+
+@pytest.mark.parametrize("name", ["mixtral", "olmoe"])
+def test_qkv_ring_geometry_is_bitwise(name):
+    """The split-K QKV GEMV streams 3 x 16-k-step ring stages by default
+    (dense_gemv_cluster_kernel, stage size a launch parameter;
+    CASCADE_QKV_STAGE_KS=8 gives the 3 x 8 ring the O projection keeps).
+    Each CTA's k-range and the order of its MMAs into TMEM do not depend on
+    the stage size, so the two rings give the same bits: checked on the
+    post-attention residual, the final logits and the acceptance of
+    prefill + verify steps of width 1, 4 and 9."""
+    import os
+
+    shape = cb.preset(name).with_layers(2)
+    m = cb.Model(shape, 7)
+    rng = np.random.default_rng(7)
+    prompt = rng.integers(0, shape.vocab, 200).astype(np.int32)
+    drafts = {k: rng.integers(0, shape.vocab, k).astype(np.int32) for k in (0, 3, 8)}
+    outs = {}
+    for arm in ("16", "8"):
+        old = os.environ.get("CASCADE_QKV_STAGE_KS")
+        os.environ["CASCADE_QKV_STAGE_KS"] = arm
+        try:
+            s = cb.Session(m, max_ctx=512, k_max=8)
+        finally:
+            if old is None:
+                os.environ.pop("CASCADE_QKV_STAGE_KS", None)
+            else:
+                os.environ["CASCADE_QKV_STAGE_KS"] = old
+        s.set_batch_invariant(True)
+        s.prefill(prompt)
+        s.enable_taps(True)
+        rec = []
+        for k in (0, 3, 8):
+            o = s.verify(drafts[k])
+            rec.append((s.tap("x_mid")[:, : k + 1].copy(), s.tap("final_logits")[: k + 1].copy(), o.accepted))
+        outs[arm] = rec
+        s.close()
+    m.close()
+    for (xa, la, aa), (xb, lb, ab) in zip(outs["16"], outs["8"]):
+        assert np.array_equal(xa.view(np.uint32), xb.view(np.uint32)), float(np.abs(xa - xb).max())
+        assert np.array_equal(la.view(np.uint32), lb.view(np.uint32)), float(np.abs(la - lb).max())
+        assert aa == ab
