@@ -696,7 +696,7 @@ struct cascade_session {
     int qkv_cluster = 0;   // cluster size of the split-K QKV GEMV (0: stream-K path)
     int pf_o = 0;          // attention CTAs (the whole grid) bulk-prefetch W_o into L2 after their wait
     int umma_no_trigger = 0;  // A/B: tcgen05 GEMVs let their dependents launch only at exit
-    int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait
+    int pf_self = 0;       // cluster GEMVs bulk-prefetch the rest of their k-range into L2 before their wait (mask: 1 QKV, 2 O)
     int dense_pf = 0;      // tcgen05 GEMVs: rolling L2 prefetch this many ring stages ahead (CASCADE_DENSE_PF)
     int cluster_stages = kUStages;  // ring depth of the split-K O projection
     int o_cluster = 0;     // same for the O projection
@@ -917,7 +917,7 @@ extern "C" int cascade_session_create(cascade_model* m, int max_ctx, int k_max, 
     s->prefetch = false;
     if (const char* v = getenv("CASCADE_L2_PREFETCH")) s->prefetch = v[0] == '1';
     if (const char* v = getenv("CASCADE_PF_O")) s->pf_o = v[0] == '1';
-    if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = v[0] == '1';
+    if (const char* v = getenv("CASCADE_PF_SELF")) s->pf_self = atoi(v) & 3;
     if (const char* v = getenv("CASCADE_DENSE_PF")) s->dense_pf = std::max(0, atoi(v));
     if (const char* v = getenv("CASCADE_UMMA_TRIGGER")) s->umma_no_trigger = v[0] == '0';
     if (const char* v = getenv("CASCADE_L2_PROLOGUE")) s->l2_prologue = atoi(v);  // 1: whole range, n > 1: first n k-steps
@@ -1239,6 +1239,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             q.ld = D.qkvd;
             q.stamp = s->stamps + 1 + 2 * l;
             q.trace = tr(1);
+            q.pf_self = s->pf_self & 1;
             q.ring_stages = s->qkv_stages;
             q.stage_ks = s->qkv_stage_ks;
             if (s->qkv_cluster) CK(launch_dense_cluster(UEPI_STORE, q, s->qkv_cluster, st));
@@ -1343,6 +1344,7 @@ static int enqueue_step(cascade_session* s, int T, int* n_kernels, Prof* prof = 
             o.out = s->x;
             o.ld = D.d;
             o.trace = tr(4);
+            o.pf_self = (s->pf_self >> 1) & 1;
             if (s->o_cluster) CK(launch_dense_cluster(UEPI_ADD, o, s->o_cluster, st));
             else CK(launch_ugemv(UEPI_ADD, o, m->num_sms, st));
         } else {
