@@ -404,6 +404,11 @@ inline ScenarioReport run_scenario(const std::vector<Verifier*>& devices, const 
     }
     for (const Policy& p : cfg.policies)
         if (p.kind == Policy::Kind::none) {
+            // a failed device cell is a runtime failure, not a missing
+            // baseline policy: name it instead of the reference's message
+            for (const CellResult& c : rep.cells)
+                if (c.failed && c.policy == "none")
+                    throw std::runtime_error("run_scenario: baseline cell " + c.task + "/none failed: " + c.error);
             compare_policies(rep);
             break;
         }
