@@ -1742,9 +1742,10 @@ extern "C" int cascade_step_kernel_count(cascade_session* s, int K, int* out) {
 extern "C" int cascade_session_reset(cascade_session* s) {
     if (!s) return set_err(CASCADE_EINVAL, "session is NULL");
     CK(cudaSetDevice(s->m->device));
+    // stream-ordered: no device-wide synchronize that would also wait on
+    // (and interleave with) other sessions' work from other host threads
+    CK(cudaMemsetAsync(s->d_state, 0, sizeof(DevState), s->stream));
     CK(cudaStreamSynchronize(s->stream));
-    CK(cudaMemset(s->d_state, 0, sizeof(DevState)));
-    CK(cudaDeviceSynchronize());
     s->len_hi = 0;
     return CASCADE_OK;
 }
@@ -1772,8 +1773,8 @@ extern "C" int cascade_set_baseline(cascade_session* s, double t_base_ns) {
 }
 
 static int read_state(cascade_session* s, DevState* out) {
+    CK(cudaMemcpyAsync(out, s->d_state, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
     CK(cudaStreamSynchronize(s->stream));
-    CK(cudaMemcpy(out, s->d_state, sizeof(DevState), cudaMemcpyDeviceToHost));
     return CASCADE_OK;
 }
 
@@ -1799,9 +1800,12 @@ extern "C" int cascade_prefill(cascade_session* s, const int32_t* prompt, int n)
         s->len_hi += T;
         pos += T;
     }
-    CK(cudaStreamSynchronize(s->stream));
+    // on the session's (non-blocking) stream: a legacy-stream copy from
+    // pageable memory may return before its DMA lands, and the next step on
+    // this stream would not wait for it
     const int32_t last = prompt[n - 1];
-    CK(cudaMemcpy(&s->d_state->pending, &last, 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(&s->d_state->pending, &last, 4, cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
     return CASCADE_OK;
 }
 
